@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py — voxelized frames/s of the B200 superquadric voxelizer.
+
+Workload (BASELINE.json config 2): synthetic frames of 2,000 superquadrics on
+the Occ3D grid 200x200x16 @0.4 m, 18 classes, tau 0.01, N=5 window, seeded
+generator of paper_2511_17361_b200/scenegen.py.  One step = one batch of
+--frames-per-step frames (default 100) through the whole path: prep ->
+scan -> emit -> radix sort -> evaluate+finalize (labels + dense v_o/v_c
+written to HBM) -> confusion counts against ground-truth labels; for N > 1
+the int64 confusion counts are all-reduced over NCCL inside the timed region.
+Frames are sharded across ranks (weak scaling: each rank runs the same number
+of frames per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line on rank 0.  --impl reference times the CPU FP64 oracle
+(oracle/, the reference's algorithm restated in C, all host threads) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxelized frames/sec (200×200×16, 18 cls, 2k SQs) at 1/2/4/8 B200; % FP32 roofline"
+UNIT = "frames/s"
+MUFU_PER_PAIR = 9      # 4 lg2 + 5 ex2 per (primitive, voxel) pair, SURVEY.md §8d
+FP32_PER_PAIR = 40     # ~21 + (C+1) FP32-pipe instructions at C = 18, SURVEY.md §8d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--frames-per-step", type=int, default=100)
+    ap.add_argument("--n-prims", type=int, default=2000)
+    ap.add_argument("--classes", type=int, default=18)
+    ap.add_argument("--seed", type=int, default=20251117)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {"workload": f"config2: synthetic frames x {a.n_prims} SQs, Occ3D 200x200x16 @0.4 m, "
+                        f"{a.classes} classes, tau 0.01, N=5 window, logit-sum",
+            "frames_per_step": a.frames_per_step, "frames_per_rank": a.frames_per_step * a.steps,
+            "n_prims": a.n_prims, "grid": [200, 200, 16], "resolution": 0.4,
+            "classes": a.classes, "generator": "scenegen.gen_frames (SPEC.md:594-597), seed "
+                                               f"{a.seed}+frame; s~U[0.2,4], eps~U[0.2,2]",
+            "outputs": "labels u8 + v_o f32 + v_c f32 written per frame; confusion vs gt",
+            "l2": "not flushed explicitly: each step writes ~4.9 GB of outputs (>> 126 MB L2)",
+            "parallelism": f"frame-sharded x{world} (no data-path collective; int64 confusion "
+                           "all-reduce over NCCL)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.idx), "-lms", "50"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9 and p[1].replace(".", "").isdigit():
+                    rows.append(p)
+        except Exception:
+            pass
+        if self.path:
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": float(rows[0][2]),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
+                if any(r[3].replace(".", "").isdigit() for r in rows) else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle: test/baseline infrastructure only)
+# ---------------------------------------------------------------------------
+
+def cpu_run(a, max_frames, budget_s):
+    """Time the FP64 oracle (all host threads) on frames of the same workload
+    until budget_s elapses or max_frames frames are done.  Returns
+    (frames/s, frames, seconds, threads, pairs/s)."""
+    from oracle import oracle as O
+    from paper_2511_17361_b200.scenegen import gen_frames
+    O.build()
+    threads = O.threads()
+    grid, cfg = O.Grid(), O.Cfg()
+    done, pairs, t_total = 0, 0, 0.0
+    while done < max_frames and (t_total < budget_s or done == 0):
+        b = O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=done))
+        t0 = time.perf_counter()
+        r = O.voxelize(b, grid, cfg)
+        t_total += time.perf_counter() - t0
+        pairs += r["n_pairs"]
+        done += 1
+    return done / t_total, done, t_total, threads, pairs / t_total
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from paper_2511_17361_b200.scenegen import gen_frames
+    from oracle import oracle as O
+    O.build()
+    grid, cfg = O.Grid(), O.Cfg()
+    frames = [O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=k))
+              for k in range(a.warmup + a.steps)]
+    for k in range(a.warmup):
+        O.voxelize(frames[k], grid, cfg)
+    t0 = time.perf_counter()
+    pairs = 0
+    for k in range(a.steps):
+        pairs += O.voxelize(frames[a.warmup + k], grid, cfg)["n_pairs"]
+    dt = time.perf_counter() - t0
+    value = a.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**workload_config(a, 1), "frames_per_step": 1,
+                       "frames_per_rank": a.steps},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.threads(), "kind": "port",
+                             "sample": f"{a.steps} frames (1 per step) of the config-2 workload, "
+                                       f"FP64 C oracle, OpenMP {O.threads()} threads; "
+                                       f"{pairs / dt:.3e} pairs/s"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+def run_ours(a, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_17361_b200 as P
+    from paper_2511_17361_b200 import _lib
+    from paper_2511_17361_b200.metrics import confusion_matrix
+    from paper_2511_17361_b200.scenegen import gen_frames, jitter
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    C, B, K, W = a.classes, a.frames_per_step, a.steps, a.warmup
+    vox = P.Voxelizer(spec, cfg, C)
+    n_batches = K
+    first = rank * n_batches * B  # disjoint frames per rank (weak scaling)
+
+    # ---- synthetic inputs (host, seeded) + ground truth (untimed) ----
+    host_batches = [gen_frames(a.seed, B, a.n_prims, C, first_frame=first + k * B)
+                    for k in range(n_batches)]
+    dev_batches = [vox.to_device(b) for b in host_batches]
+    gt = []
+    for k, b in enumerate(host_batches):
+        r = vox(jitter(b, seed=a.seed + 7919 + first + k), dense=False)
+        gt.append(r.labels.clone())
+    out = vox.alloc(B, dense=True)
+    K1 = C + 1
+    cm = torch.zeros((K1, K1), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- measured pipe peaks (roofline denominators) ----
+    mufu_peak = _lib.microbench(0)
+    ffma_peak = _lib.microbench(1)
+
+    # ---- warm-up ----
+    for k in range(W):
+        vox(dev_batches[k % n_batches], out=out)
+        confusion_matrix(out.labels, gt[k % n_batches], C, out=cm)
+    barrier()
+
+    # ---- timed: device-resident inputs ----
+    cm.zero_()
+    _lib.profile_enable(True)
+    _lib.profile_read(reset=True)
+    n_launch0 = _lib.launch_count()
+    pairs = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for k in range(K):
+            r = vox(dev_batches[k % n_batches], out=out)
+            pairs += r.n_pairs
+            confusion_matrix(out.labels, gt[k % n_batches], C, out=cm)
+        if world > 1:
+            dist.all_reduce(cm, op=dist.ReduceOp.SUM)
+        ev1.record(stream)
+        barrier()
+    clocks = clk.summary()
+    launches = _lib.launch_count() - n_launch0
+    prof = _lib.profile_read(reset=True)
+    _lib.profile_enable(False)
+    dt = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
+    frames_total = world * K * B
+    value = frames_total / dt
+    pairs_total = max_over_ranks(float(pairs))  # identical workload shape per rank
+
+    # roofline of the dominant kernel (eval_kernel): algorithmic MUFU ops per
+    # launch / its CUDA-event duration inside the timed region
+    eval_s = prof["eval_ms"] * 1e-3 / max(prof["calls"], 1)
+    pairs_per_launch = pairs / max(K, 1)
+    achieved = pairs_per_launch * MUFU_PER_PAIR / eval_s
+    roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
+                "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": None,
+                "kernel": f"eval_kernel<{vox.C if vox.C in (2, 4, 8, 12, 16, 18, 24, 32) else 'cm'}>",
+                "algorithmic": f"{MUFU_PER_PAIR} MUFU per in-window (primitive, voxel) pair x "
+                               f"{pairs_per_launch:.4e} pairs per launch",
+                "eval_ms_per_launch": eval_s * 1e3,
+                "eval_share_of_step": prof["eval_ms"] / max(1e-9, dt * 1e3),
+                "stage_ms_per_step": {k: v / max(prof["calls"], 1) for k, v in prof.items()
+                                      if k.endswith("_ms")},
+                "peak_source": "sqv_microbench(MUFU) measured live on this GPU",
+                "fp32_pipe": {"achieved_glanes": pairs_per_launch * FP32_PER_PAIR / eval_s / 1e9,
+                              "peak_glanes": ffma_peak / 1e9,
+                              "frac": pairs_per_launch * FP32_PER_PAIR / eval_s / ffma_peak}}
+
+    # ---- e2e: public API from pinned host buffers, labels back to host ----
+    e2e = None
+    if not a.no_e2e:
+        pinned = []
+        for b in host_batches:
+            f = {k: torch.from_numpy(np.ascontiguousarray(getattr(b, k))).pin_memory()
+                 for k in P.PrimitiveBatch.FIELDS}
+            pinned.append(P.PrimitiveBatch(**f))
+        lab_host = torch.empty(out.labels.shape, dtype=torch.uint8).pin_memory()
+        cm_host = torch.empty(cm.shape, dtype=torch.int64).pin_memory()
+        h2d = sum(getattr(pinned[0], k).numel() * 8 for k in P.PrimitiveBatch.FIELDS)
+        d2h = lab_host.numel()
+        for k in range(min(W, 2)):
+            vox(pinned[k % n_batches], out=out)
+        barrier()
+        cm.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for k in range(K):
+            vox(pinned[k % n_batches], out=out)
+            confusion_matrix(out.labels, gt[k % n_batches], C, out=cm)
+            lab_host.copy_(out.labels, non_blocking=True)
+        if world > 1:
+            dist.all_reduce(cm, op=dist.ReduceOp.SUM)
+        cm_host.copy_(cm, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        dt_e2e = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+        e2e = {"value": frames_total / dt_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "wall_s": max_over_ranks(wall),
+               "path": "Voxelizer.__call__ on pinned host PrimitiveBatch (H2D inside) -> "
+                       "confusion -> labels D2H to pinned host, per step"}
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        fps, nfr, secs, thr, pps = cpu_run(a, 8, a.cpu_seconds)
+        cpu = {"value": fps, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"{nfr} frames of the config-2 workload in {secs:.1f} s, FP64 C oracle "
+                         f"(oracle/sqv_oracle.c), OpenMP {thr} threads; {pps:.3e} pairs/s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 prep)",
+                "data": "synthetic", "config": workload_config(a, world),
+                "pairs_per_s": world * pairs_total / dt, "gpu_launches": launches,
+                "roofline": roofline, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+                "confusion_total": int(cm.sum().item())}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

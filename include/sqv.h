@@ -25,7 +25,8 @@
  *   - Return value: SQV_OK (0) or a negative SQV_ERR_* code; a message is
  *     available from sqv_last_error() (thread-local).
  *   - The library never allocates device memory and keeps no global mutable
- *     state besides the thread-local error string and a launch counter.
+ *     state besides the thread-local error string, a launch counter and the
+ *     opt-in stage profiler (sqv_profile_*).
  *     Scratch comes from the caller's workspace pointer.
  *   - Results are deterministic: identical inputs give bit-identical outputs
  *      regardless of batch composition or GPU count.
@@ -169,6 +170,21 @@ int sqv_confusion(const uint8_t* pred, const uint8_t* gt, int64_t n_voxels, int3
  */
 int sqv_density(const sqv_prims* prims, const double* points, const int32_t* pair_prim,
                 int64_t n_points, float* F, float* density, void* stream);
+
+/* ---- instrumentation (bench / profiling; not part of the reference API) ----
+ * When enabled, sqv_voxelize records CUDA events around its device stages on
+ * the caller's stream and accumulates their durations:
+ *   ms[0] prep + count scan, ms[1] emit + radix sort + tile scan,
+ *   ms[2] evaluate + finalize (the hot kernel), ms[3] sum of the three.
+ * sqv_profile_read synchronises the pending events; reset != 0 zeroes. */
+#define SQV_NSTAGES 4
+int sqv_profile_enable(int on);
+int sqv_profile_read(double* ms, int64_t* calls, int reset);
+
+/* Microbenchmarks of the pipes that bound the evaluator (roofline
+ * denominators measured on the running GPU): which = 0 -> MUFU (SFU) ex2/lg2
+ * ops/s, 1 -> FP32 FFMA lanes/s.  *ops_per_s receives the achieved rate. */
+int sqv_microbench(int which, double* ops_per_s, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,414 @@
+// sqv_api.cu — the C ABI of include/sqv.h: argument checks, workspace
+// layout, and the stage sequence of sqv_voxelize.
+#include <atomic>
+#include <mutex>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "sqv_kernels.cuh"
+
+namespace sqv {
+
+static std::atomic<long long> g_launches{0};
+static thread_local char g_err[512] = "";
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SQV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return SQV_OK;
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Header {  // device-side scalars, read back in one 32-byte copy
+  long long n_entries;
+  unsigned long long bad_word;
+  unsigned long long n_pairs;
+  long long pad;
+};
+
+struct Layout {
+  size_t hdr, recs, lrows, counts, offs, windows, tile_cnt, tile_off, scan_tmp;  // fixed
+  size_t keys_a, vals_a, keys_b, vals_b, radix_tmp;                              // variable
+  size_t fixed_end, total;
+};
+
+Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
+  Layout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += up(bytes);
+    return at;
+  };
+  L.hdr = take(sizeof(Header));
+  L.recs = take((size_t)FN * kRecWords * 4);
+  L.lrows = take((size_t)FN * lrow * 4);
+  L.counts = take((size_t)(FN + 1) * 4);
+  L.offs = take((size_t)(FN + 1) * 4);
+  L.windows = take((size_t)FN * 6 * 4);
+  L.tile_cnt = take((size_t)(FT + 1) * 4);
+  L.tile_off = take((size_t)(FT + 1) * 4);
+  const int64_t st = scan_tmp_ints(FN > FT ? FN : FT);
+  L.scan_tmp = take((size_t)st * 4);
+  L.fixed_end = o;
+  L.keys_a = take((size_t)n_entries * 4);
+  L.vals_a = take((size_t)n_entries * 4);
+  L.keys_b = take((size_t)n_entries * 4);
+  L.vals_b = take((size_t)n_entries * 4);
+  L.radix_tmp = take((size_t)radix_tmp_ints(n_entries) * 4);
+  L.total = o;
+  return L;
+}
+
+int check_grid(const sqv_grid* g) {
+  if (!g) return set_error(SQV_ERR_ARG, "grid is NULL");
+  for (int k = 0; k < 3; ++k) {
+    if (g->dims[k] < 1) return set_error(SQV_ERR_ARG, "dims must be >= 1");
+    if (!std::isfinite(g->origin[k])) return set_error(SQV_ERR_ARG, "origin must be finite");
+  }
+  if (!(g->resolution > 0.0) || !std::isfinite(g->resolution))
+    return set_error(SQV_ERR_ARG, "resolution must be > 0");
+  const int64_t V = (int64_t)g->dims[0] * g->dims[1] * g->dims[2];
+  if (V > (1LL << 40)) return set_error(SQV_ERR_ARG, "grid too large");
+  return SQV_OK;
+}
+
+void tiles_of(const sqv_grid* g, int* ntx, int* nty, int* ntz) {
+  *ntx = (g->dims[0] + kTileX - 1) / kTileX;
+  *nty = (g->dims[1] + kTileY - 1) / kTileY;
+  *ntz = (g->dims[2] + kTileZ - 1) / kTileZ;
+}
+
+// tau compared in FP32 exactly as FP64 v_o < tau would be for an FP32 v_o:
+// the smallest float >= tau.
+float tau_f32(double tau) {
+  if (std::isinf(tau)) return tau > 0 ? INFINITY : -INFINITY;
+  float t = (float)tau;
+  if ((double)t < tau) t = std::nextafter(t, INFINITY);
+  return t;
+}
+
+// Opt-in stage profiler (sqv_profile_*): CUDA events on the caller's stream.
+// The previous call's emit/sort/eval events are folded in at the next
+// call's header readback (stream order guarantees they completed).
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  bool pending = false;
+  bool created = false;
+  cudaEvent_t ev[5];
+  double ms[SQV_NSTAGES] = {0, 0, 0, 0};
+  long long calls = 0;
+  void ensure() {
+    if (!created) {
+      for (auto& e : ev) cudaEventCreate(&e);
+      created = true;
+    }
+  }
+  static float el(cudaEvent_t a, cudaEvent_t b) {
+    float m = 0.f;
+    cudaEventElapsedTime(&m, a, b);
+    return m;
+  }
+  void fold_pending() {
+    if (!pending) return;
+    const double m1 = el(ev[2], ev[3]), m2 = el(ev[3], ev[4]);
+    ms[1] += m1;
+    ms[2] += m2;
+    ms[3] += m1 + m2;
+    pending = false;
+  }
+};
+Profiler g_prof;
+
+}  // namespace
+}  // namespace sqv
+
+using namespace sqv;
+
+extern "C" {
+
+int sqv_abi_version(void) { return SQV_ABI_VERSION; }
+const char* sqv_last_error(void) { return g_err; }
+int64_t sqv_launch_count(void) { return g_launches.load(); }
+
+int64_t sqv_tiles_per_frame(const sqv_grid* grid) {
+  if (check_grid(grid)) return -1;
+  int a, b, c;
+  tiles_of(grid, &a, &b, &c);
+  return (int64_t)a * b * c;
+}
+
+size_t sqv_workspace_bytes(int32_t n_frames, int32_t n_prims, int32_t n_classes,
+                           const sqv_grid* grid, int64_t n_entries) {
+  if (check_grid(grid) || n_frames < 0 || n_prims < 0) return 0;
+  const int cm = eval_cm_for(n_classes);
+  if (!cm) return 0;
+  const int lrow = (cm + 1 + 3) & ~3;
+  const int64_t T = sqv_tiles_per_frame(grid);
+  return layout((int64_t)n_frames * n_prims, (int64_t)n_frames * T, lrow, n_entries).total;
+}
+
+int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cfg,
+                 const sqv_outputs* out, sqv_bins* bins, void* workspace, size_t ws_bytes,
+                 size_t* ws_needed, int64_t* bad_prim, int32_t* bad_bits, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (bad_prim) *bad_prim = -1;
+  if (bad_bits) *bad_bits = 0;
+  if (!prims || !cfg || !out || !out->labels) return set_error(SQV_ERR_ARG, "NULL argument");
+  if (int rc = check_grid(grid)) return rc;
+  const int F = prims->n_frames, N = prims->n_prims, C = prims->n_classes;
+  if (F < 0 || N < 0) return set_error(SQV_ERR_ARG, "negative frame/primitive count");
+  if (C < 1) return set_error(SQV_ERR_ARG, "need at least one class");
+  const int cm = eval_cm_for(C);
+  if (!cm) return set_error(SQV_ERR_UNSUPPORTED, "%d classes > SQV_MAX_CLASSES (%d)", C,
+                            SQV_MAX_CLASSES);
+  if (!(cfg->tau >= 0.0)) return set_error(SQV_ERR_ARG, "tau must be >= 0");
+  if (cfg->neighborhood_radius < 0) return set_error(SQV_ERR_ARG, "radius must be >= 0");
+  if (!(cfg->window_extent >= 0.0) || !std::isfinite(cfg->window_extent))
+    return set_error(SQV_ERR_ARG, "window_extent must be finite and >= 0");
+  if (cfg->free_label < 0 || cfg->free_label > 255 || cfg->free_label < C)
+    return set_error(SQV_ERR_ARG, "free_label must lie in [C, 255]");
+  if (cfg->semantic_mode != 0 && cfg->semantic_mode != 1)
+    return set_error(SQV_ERR_ARG, "semantic_mode must be 0 (logit-sum) or 1 (prob-sum)");
+  if (F == 0) return SQV_OK;
+  int ntx, nty, ntz;
+  tiles_of(grid, &ntx, &nty, &ntz);
+  const int64_t T = (int64_t)ntx * nty * ntz;
+  const int64_t FN = (int64_t)F * N, FT = (int64_t)F * T;
+  if (FT >= (1LL << 31) || FN >= (1LL << 31))
+    return set_error(SQV_ERR_ARG, "batch too large (split frames)");
+  const int lrow = (cm + 1 + 3) & ~3;
+  Layout L = layout(FN, FT, lrow, 0);
+  if (ws_bytes < L.fixed_end || !workspace) {
+    if (ws_needed) *ws_needed = L.total;
+    return set_error(SQV_ERR_WORKSPACE, "workspace too small: need >= %zu bytes", L.total);
+  }
+  char* ws = (char*)workspace;
+  Header* hdr = (Header*)(ws + L.hdr);
+  int* counts = (int*)(ws + L.counts);
+  int* offs = (int*)(ws + L.offs);
+  int* windows = (int*)(ws + L.windows);
+  int* tile_cnt = (int*)(ws + L.tile_cnt);
+  int* tile_off = (int*)(ws + L.tile_off);
+  int* scan_tmp = (int*)(ws + L.scan_tmp);
+  float* recs = (float*)(ws + L.recs);
+  float* lrows = (float*)(ws + L.lrows);
+
+  Header h0;
+  std::memset(&h0, 0, sizeof(h0));
+  h0.bad_word = ~0ULL;
+  if (cudaMemcpyAsync(hdr, &h0, sizeof(h0), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemsetAsync(tile_cnt, 0, (size_t)(FT + 1) * 4, s) != cudaSuccess)
+    return check_launch("workspace init");
+
+  const bool prof = g_prof.on;
+  if (prof) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.ensure();
+    cudaEventRecord(g_prof.ev[0], s);
+  }
+  // K1 prep
+  if (FN > 0) {
+    PrepArgs P;
+    P.mu = prims->mu;
+    P.scale = prims->scale;
+    P.rot = prims->rot;
+    P.opacity = prims->opacity;
+    P.eps = prims->eps;
+    P.logits = prims->logits;
+    P.n_valid = prims->n_valid;
+    P.n_frames = F;
+    P.n_prims = N;
+    P.n_classes = C;
+    P.cm = cm;
+    P.lrow = lrow;
+    P.grid = *grid;
+    P.cfg = *cfg;
+    P.recs = recs;
+    P.lrows = lrows;
+    P.counts = counts;
+    P.windows = windows;
+    P.bad_word = &hdr->bad_word;
+    P.n_pairs = &hdr->n_pairs;
+    prep_kernel<<<div_up(FN, 128), 128, 0, s>>>(P);
+    count_launch();
+    if (int rc = check_launch("prep_kernel")) return rc;
+  }
+  // K2 scan of per-primitive tile counts -> entry offsets, total -> header
+  if (int rc = scan_exclusive(counts, offs, FN, scan_tmp, &hdr->n_entries, s)) return rc;
+  if (prof) cudaEventRecord(g_prof.ev[1], s);
+  Header h;
+  if (cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return check_launch("header readback");
+  if (prof) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.fold_pending();
+    const double m0 = Profiler::el(g_prof.ev[0], g_prof.ev[1]);
+    g_prof.ms[0] += m0;
+    g_prof.ms[3] += m0;
+    g_prof.calls++;
+  }
+  if (h.bad_word != ~0ULL) {
+    if (bad_prim) *bad_prim = (int64_t)(h.bad_word >> 8);
+    if (bad_bits) *bad_bits = (int32_t)(h.bad_word & 255u);
+    return set_error(SQV_ERR_INVALID_PRIM, "primitive %lld failed validation (bits %d)",
+                     (long long)(h.bad_word >> 8), (int)(h.bad_word & 255u));
+  }
+  const int64_t E = h.n_entries;
+  if (E >= (1LL << 31) - 1) return set_error(SQV_ERR_ARG, "too many bin entries (split frames)");
+  L = layout(FN, FT, lrow, E);
+  if (ws_needed) *ws_needed = L.total;
+  if (ws_bytes < L.total)
+    return set_error(SQV_ERR_WORKSPACE, "workspace too small: need %zu bytes", L.total);
+  uint32_t* keys_a = (uint32_t*)(ws + L.keys_a);
+  uint32_t* keys_b = (uint32_t*)(ws + L.keys_b);
+  int* vals_a = (int*)(ws + L.vals_a);
+  int* vals_b = (int*)(ws + L.vals_b);
+  int* radix_tmp = (int*)(ws + L.radix_tmp);
+
+  if (prof) cudaEventRecord(g_prof.ev[2], s);
+  // K3 emit + K4 radix sort + tile offsets
+  int which = 0;
+  if (E > 0) {
+    EmitArgs Em;
+    Em.n_frames = F;
+    Em.n_prims = N;
+    Em.tiles_per_frame = (int)T;
+    Em.ntx = ntx;
+    Em.nty = nty;
+    Em.counts = counts;
+    Em.offs = offs;
+    Em.windows = windows;
+    Em.keys = keys_a;
+    Em.vals = vals_a;
+    Em.tile_cnt = tile_cnt;
+    emit_kernel<<<div_up(FN, 128), 128, 0, s>>>(Em);
+    count_launch();
+    if (int rc = check_launch("emit_kernel")) return rc;
+    int bits = 0;
+    while (bits < 32 && (1LL << bits) < FT) ++bits;
+    if (int rc = radix_sort(keys_a, vals_a, keys_b, vals_b, E, bits, radix_tmp, &which, s))
+      return rc;
+  }
+  if (int rc = scan_exclusive(tile_cnt, tile_off, FT, scan_tmp, nullptr, s)) return rc;
+  const int* sorted_vals = which ? vals_b : vals_a;
+
+  // K5 evaluate + finalize
+  EvalArgs A;
+  A.recs = recs;
+  A.lrows = lrows;
+  A.tile_off = tile_off;
+  A.prim_ids = sorted_vals;
+  A.n_prims = N;
+  A.n_classes = C;
+  A.lrow = lrow;
+  A.tiles_per_frame = (int)T;
+  A.ntx = ntx;
+  A.nty = nty;
+  A.nx = grid->dims[0];
+  A.ny = grid->dims[1];
+  A.nz = grid->dims[2];
+  A.tau = tau_f32(cfg->tau);
+  A.free_label = cfg->free_label;
+  A.labels = out->labels;
+  A.v_o = out->v_o;
+  A.v_c = out->v_c;
+  if (prof) cudaEventRecord(g_prof.ev[3], s);
+  if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
+  if (prof) {
+    cudaEventRecord(g_prof.ev[4], s);
+    g_prof.pending = true;
+  }
+
+  if (bins) {
+    bins->n_entries = E;
+    bins->n_pairs = (int64_t)h.n_pairs;
+    if (bins->windows &&
+        cudaMemcpyAsync(bins->windows, windows, (size_t)FN * 6 * 4, cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess)
+      return check_launch("bins export");
+    if (bins->tile_off &&
+        cudaMemcpyAsync(bins->tile_off, tile_off, (size_t)(FT + 1) * 4, cudaMemcpyDeviceToDevice,
+                        s) != cudaSuccess)
+      return check_launch("bins export");
+    if (bins->prim_ids) {
+      if (bins->capacity < E)
+        return set_error(SQV_ERR_CAPACITY, "bins capacity %lld < %lld entries",
+                         (long long)bins->capacity, (long long)E);
+      if (E > 0 && cudaMemcpyAsync(bins->prim_ids, sorted_vals, (size_t)E * 4,
+                                   cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return check_launch("bins export");
+    }
+  }
+  return SQV_OK;
+}
+
+int sqv_finalize(const float* v_o, const float* v_c, int64_t n_voxels, int32_t n_classes,
+                 double tau, int32_t free_label, uint8_t* labels, void* stream) {
+  if (n_voxels < 0 || n_classes < 1 || !(tau >= 0.0) || free_label < n_classes ||
+      free_label > 255)
+    return set_error(SQV_ERR_ARG, "invalid finalize arguments");
+  return finalize_launch(v_o, v_c, n_voxels, n_classes, tau_f32(tau), free_label, labels,
+                         (cudaStream_t)stream);
+}
+
+int sqv_confusion(const uint8_t* pred, const uint8_t* gt, int64_t n_voxels, int32_t n_classes,
+                  int32_t free_label, int64_t* cm, void* stream) {
+  (void)free_label;  // every label >= C (free_label included) maps to index C
+  if (n_voxels < 0 || n_classes < 1 || n_classes > 255)
+    return set_error(SQV_ERR_ARG, "invalid confusion arguments");
+  return confusion_launch(pred, gt, n_voxels, n_classes, cm, (cudaStream_t)stream);
+}
+
+int sqv_density(const sqv_prims* prims, const double* points, const int32_t* pair_prim,
+                int64_t n_points, float* F, float* density, void* stream) {
+  if (!prims || n_points < 0) return set_error(SQV_ERR_ARG, "invalid density arguments");
+  return density_launch(prims, points, pair_prim, n_points, F, density, (cudaStream_t)stream);
+}
+
+int sqv_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on != 0;
+  return SQV_OK;
+}
+
+int sqv_profile_read(double* ms, int64_t* calls, int reset) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (g_prof.pending) {
+    cudaEventSynchronize(g_prof.ev[4]);
+    g_prof.fold_pending();
+  }
+  if (ms)
+    for (int k = 0; k < SQV_NSTAGES; ++k) ms[k] = g_prof.ms[k];
+  if (calls) *calls = g_prof.calls;
+  if (reset) {
+    for (int k = 0; k < SQV_NSTAGES; ++k) g_prof.ms[k] = 0.0;
+    g_prof.calls = 0;
+  }
+  return SQV_OK;
+}
+
+int sqv_microbench(int which, double* ops_per_s, void* stream) {
+  if (!ops_per_s || (which != 0 && which != 1)) return set_error(SQV_ERR_ARG, "microbench args");
+  return microbench(which, ops_per_s, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// sqv_common.cuh — shared device code of libsqv (B200 / sm_100a).
+//
+// Per-primitive FP64 setup (the reference's SuperQuadric.__post_init__ +
+// world_to_local_matrix + the SPEC window), the FP32 inside-outside field on
+// the SFU (MUFU.LG2 / MUFU.EX2), and the launch bookkeeping.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sqv.h"
+
+namespace sqv {
+
+// ---- constants ---------------------------------------------------------
+
+constexpr double kEpsMin = 0.2;  // core.py:18
+constexpr double kEpsMax = 2.0;  // core.py:19
+constexpr float kFCap = 1e30f;   // core.py:23 (reported F only)
+// exp(-F) underflows FP32 (flush-to-zero) for F > 126*ln2 = 87.3365.  The
+// evaluator writes w = 0 exactly for F >= kFCut, so culling by a
+// conservative lower bound of F never changes a single output bit.
+constexpr float kFCut = 87.3365f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
+
+// Per-primitive evaluation record (FP32, 36 words = 9 x float4).
+//   H[r][j], L[r][j]: hi/lo split of res * M'[r][j], M' = diag(1/s) * Rwl
+//   G[r]:             local (scaled) coords of the reference voxel centre
+//   a, b, c:          2/eps2, eps2/eps1, 2/eps1 (core.py:267-269)
+//   mcut:             Chebyshev cull bound, F >= max|x'|^(2/eps1)
+//   cx, cy, cz:       reference voxel index (exact small integers)
+//   lo[3], hi[3]:     clipped voxel window (int)
+//   sigma:            opacity
+constexpr int kRecWords = 36;
+struct __align__(16) PrimRec {
+  float H[9];
+  float L[9];
+  float G[3];
+  float a, b, c;
+  float mcut;
+  float cx, cy, cz;
+  int lo[3];
+  int hi[3];
+  float sigma;
+  float pad;
+};
+static_assert(sizeof(PrimRec) == kRecWords * 4, "PrimRec layout");
+
+// ---- MUFU wrappers -----------------------------------------------------
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Inside-outside field (core.py:270): F = (|x|^a + |y|^a)^b + |z|^c with the
+// 1/s scaling already folded into the local coordinates.  9 SFU ops per call
+// including the caller's exp.  x = 0 gives lg2 = -inf -> ex2 = 0 exactly; a
+// saturated power gives +inf, which fails the F < kFCut test (w = 0), so no
+// NaN can arise from valid inputs.
+__device__ __forceinline__ float field_F(float x0, float x1, float x2, float a, float b,
+                                         float c) {
+  const float X = ex2(a * lg2(fabsf(x0)));
+  const float Y = ex2(a * lg2(fabsf(x1)));
+  const float Sb = ex2(b * lg2(X + Y));
+  const float Z = ex2(c * lg2(fabsf(x2)));
+  return Sb + Z;
+}
+
+__device__ __forceinline__ float density_of(float F) {
+  return F < kFCut ? ex2(-F * kLog2e) : 0.0f;
+}
+
+// ---- FP64 per-primitive setup ------------------------------------------
+
+struct PrimF64 {
+  double mu[3];
+  double M[9];  // diag(1/s) * world_to_local, row-major
+  double e1, e2;
+  double sigma;
+  double smax;
+  int bad;
+};
+
+// Validation (core.py:147-159, 33-34) in the same order, normalisation and
+// eps clamp (core.py:160-165), world_to_local = quat_to_matrix(q)^T
+// (core.py:55-65,183-185), scaled by 1/s (core.py:264-266).
+__device__ inline PrimF64 prim_setup(const double* mu, const double* scale, const double* rot,
+                                     double opacity, const double* eps, const double* logits,
+                                     int C) {
+  PrimF64 P;
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (!isfinite(mu[k]) || !isfinite(scale[k])) bad |= SQV_BAD_MU_SCALE_FINITE;
+  if (!bad) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (!(scale[k] > 0.0)) bad |= SQV_BAD_SCALE_POSITIVE;
+  }
+  for (int k = 0; k < C; ++k)
+    if (!isfinite(logits[k])) bad |= SQV_BAD_LOGITS_FINITE;
+  if (!(opacity >= 0.0 && opacity <= 1.0)) bad |= SQV_BAD_OPACITY;
+  const double qw = rot[0], qx = rot[1], qy = rot[2], qz = rot[3];
+  const double n = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  if (!(n >= 1e-12)) bad |= SQV_BAD_QUAT;
+  if (!isfinite(eps[0]) || !isfinite(eps[1])) bad |= SQV_BAD_EPS;
+  P.bad = bad;
+  if (bad) return P;
+  const double w = qw / n, x = qx / n, y = qy / n, z = qz / n;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double wx = w * x, wy = w * y, wz = w * z;
+  const double xy = x * y, xz = x * z, yz = y * z;
+  // local-to-world R (core.py:60-64); world-to-local is R^T
+  const double R[9] = {1.0 - 2.0 * (yy + zz), 2.0 * (xy - wz), 2.0 * (xz + wy),
+                       2.0 * (xy + wz), 1.0 - 2.0 * (xx + zz), 2.0 * (yz - wx),
+                       2.0 * (xz - wy), 2.0 * (yz + wx), 1.0 - 2.0 * (xx + yy)};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) P.M[3 * r + j] = R[3 * j + r] / scale[r];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) P.mu[k] = mu[k];
+  P.e1 = fmin(fmax(eps[0], kEpsMin), kEpsMax);
+  P.e2 = fmin(fmax(eps[1], kEpsMin), kEpsMax);
+  P.sigma = opacity;
+  P.smax = fmax(fmax(scale[0], scale[1]), scale[2]);
+  return P;
+}
+
+// ---- launch bookkeeping --------------------------------------------------
+
+void count_launch();
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace sqv

@@ -1,0 +1,79 @@
+// sqv_kernels.cuh — kernel argument blocks and host-side launchers.
+#pragma once
+
+#include "sqv_common.cuh"
+
+namespace sqv {
+
+struct PrepArgs {
+  const double *mu, *scale, *rot, *opacity, *eps, *logits;
+  const int32_t* n_valid;
+  int n_frames, n_prims, n_classes;
+  int cm;    // padded class count of the evaluator instantiation (sigma at lrow[cm])
+  int lrow;  // floats per class-weight row
+  sqv_grid grid;
+  sqv_cfg cfg;
+  float* recs;   // [FN][kRecWords]
+  float* lrows;  // [FN][lrow]
+  int* counts;   // [FN] tiles overlapped
+  int* windows;  // [FN][6]
+  unsigned long long* bad_word;
+  unsigned long long* n_pairs;
+};
+
+struct EmitArgs {
+  int n_frames, n_prims;
+  int tiles_per_frame, ntx, nty;
+  const int* counts;
+  const int* offs;
+  const int* windows;
+  uint32_t* keys;
+  int* vals;
+  int* tile_cnt;
+};
+
+struct EvalArgs {
+  const float* recs;
+  const float* lrows;
+  const int* tile_off;
+  const int* prim_ids;
+  int n_prims, n_classes, lrow;
+  int tiles_per_frame, ntx, nty;
+  int nx, ny, nz;
+  float tau;
+  int free_label;
+  uint8_t* labels;
+  float* v_o;
+  float* v_c;
+};
+
+__global__ void prep_kernel(PrepArgs A);
+__global__ void emit_kernel(EmitArgs A);
+
+// exclusive scan of n int32 values; out has n+1 entries (out[n] = total);
+// if total64 != nullptr the total is also stored there.  tmp needs
+// scan_tmp_ints(n) ints.
+int64_t scan_tmp_ints(int64_t n);
+int scan_exclusive(const int* in, int* out, int64_t n, int* tmp, long long* total64,
+                   cudaStream_t s);
+
+// stable LSD radix sort of (keys, vals) by the low `bits` bits of key.
+// Result lands in (keys, vals) or (keys_alt, vals_alt); returns 0 or 1 in *which.
+int64_t radix_tmp_ints(int64_t n);
+int radix_sort(uint32_t* keys, int* vals, uint32_t* keys_alt, int* vals_alt, int64_t n, int bits,
+               int* tmp, int* which, cudaStream_t s);
+
+// evaluator
+int eval_cm_for(int C);  // padded class count for C (0 if unsupported)
+int eval_launch(const EvalArgs& A, int cm, int n_tiles_total, cudaStream_t s);
+
+// misc kernels
+int finalize_launch(const float* v_o, const float* v_c, int64_t n, int C, float tau, int free_label,
+                    uint8_t* labels, cudaStream_t s);
+int confusion_launch(const uint8_t* pred, const uint8_t* gt, int64_t n, int C, int64_t* cm,
+                     cudaStream_t s);
+int microbench(int which, double* ops_per_s, cudaStream_t s);
+int density_launch(const sqv_prims* P, const double* points, const int32_t* pair_prim,
+                   int64_t n, float* F, float* density, cudaStream_t s);
+
+}  // namespace sqv

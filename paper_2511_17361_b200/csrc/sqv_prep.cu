@@ -1,0 +1,171 @@
+// sqv_prep.cu — K1 per-primitive preparation and K3 bin emission.
+//
+// K1 (one thread per (frame, primitive), FP64): validation, quaternion
+// normalisation, eps clamp (core.py:143-173), scaled world->local matrix
+// (core.py:183-185, 264-266), the SPEC voxel window (ledger
+// SPEC.md:382) evaluated with the same IEEE expressions as the oracle, the
+// overlapped-tile count, and the FP32 evaluation record (PrimRec) the tile
+// evaluator consumes.
+//
+// K3 (one thread per primitive): writes one (tile key, primitive) entry per
+// overlapped tile, in primitive order, and counts entries per tile.
+#include "sqv_common.cuh"
+#include "sqv_kernels.cuh"
+
+namespace sqv {
+
+// Split v (FP64) into hi + lo where every hi of the row is a multiple of the
+// row quantum q (10 significant bits of the row's largest entry).  Then
+// k * hi is exact for |k| < 2^12 and the sum of the three hi products of a
+// row is exact in FP32, so lattice offsets never cancel catastrophically.
+__device__ inline void split_row(const double v[3], float hi[3], float lo[3]) {
+  const double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fabs(v[2]));
+  if (m == 0.0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) hi[j] = lo[j] = 0.0f;
+    return;
+  }
+  int e;
+  frexp(m, &e);                       // m in [2^(e-1), 2^e)
+  const double q = ldexp(1.0, e - 10);
+  const double iq = ldexp(1.0, 10 - e);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double h = rint(v[j] * iq) * q;
+    hi[j] = (float)h;                 // exact: <= 11 significant bits
+    lo[j] = (float)(v[j] - h);
+  }
+}
+
+__global__ void prep_kernel(PrepArgs A) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t FN = (int64_t)A.n_frames * A.n_prims;
+  if (gi >= FN) return;
+  const int f = (int)(gi / A.n_prims);
+  const int i = (int)(gi - (int64_t)f * A.n_prims);
+  const int C = A.n_classes;
+  PrimRec rec;
+  float* rw = reinterpret_cast<float*>(&rec);
+#pragma unroll
+  for (int k = 0; k < kRecWords; ++k) rw[k] = 0.0f;
+  rec.lo[0] = rec.lo[1] = rec.lo[2] = 1;
+  rec.hi[0] = rec.hi[1] = rec.hi[2] = 0;
+  int count = 0;
+  float* lrow = A.lrows + gi * A.lrow;
+  for (int k = 0; k < A.lrow; ++k) lrow[k] = 0.0f;
+
+  const bool valid_slot = !A.n_valid || i < A.n_valid[f];
+  if (valid_slot) {
+    const double* logits = A.logits + gi * C;
+    PrimF64 P = prim_setup(A.mu + 3 * gi, A.scale + 3 * gi, A.rot + 4 * gi, A.opacity[gi],
+                           A.eps + 2 * gi, logits, C);
+    if (P.bad) {
+      // first failing primitive wins: min over (index << 8 | bits)
+      atomicMin(A.bad_word, ((unsigned long long)gi << 8) | (unsigned long long)P.bad);
+    } else {
+      // ---- window; identical expressions to the oracle ----
+      double lo[3], hi[3], cc[3];
+      const double res = A.grid.resolution;
+      const double r = (double)A.cfg.neighborhood_radius +
+                       ceil(__ddiv_rn(__dmul_rn(P.smax, A.cfg.window_extent), res));
+      bool empty = false;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        cc[k] = floor(__ddiv_rn(__dsub_rn(P.mu[k], A.grid.origin[k]), res));
+        if (A.cfg.truncate) {
+          lo[k] = fmax(__dsub_rn(cc[k], r), 0.0);
+          hi[k] = fmin(__dadd_rn(cc[k], r), (double)(A.grid.dims[k] - 1));
+        } else {
+          lo[k] = 0.0;
+          hi[k] = (double)(A.grid.dims[k] - 1);
+        }
+        empty |= lo[k] > hi[k];
+      }
+      if (!empty && P.sigma > 0.0) {  // sigma = 0 primitives are skipped
+        int ilo[3], ihi[3];
+        int64_t vol = 1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ilo[k] = (int)lo[k];
+          ihi[k] = (int)hi[k];
+          rec.lo[k] = ilo[k];
+          rec.hi[k] = ihi[k];
+          vol *= (int64_t)(ihi[k] - ilo[k] + 1);
+        }
+        count = (ihi[0] / kTileX - ilo[0] / kTileX + 1) * (ihi[1] / kTileY - ilo[1] / kTileY + 1) *
+                (ihi[2] / kTileZ - ilo[2] / kTileZ + 1);
+        atomicAdd(A.n_pairs, (unsigned long long)vol);
+        // ---- evaluation record ----
+        // reference voxel: the centre voxel clamped into the window, so that
+        // lattice offsets k = idx - cref stay small integers.
+        double cref[3], d[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          cref[k] = fmin(fmax(cc[k], lo[k]), hi[k]);
+          d[k] = (A.grid.origin[k] + (cref[k] + 0.5) * res) - P.mu[k];
+        }
+#pragma unroll
+        for (int r2 = 0; r2 < 3; ++r2) {
+          const double row[3] = {P.M[3 * r2] * res, P.M[3 * r2 + 1] * res, P.M[3 * r2 + 2] * res};
+          split_row(row, &rec.H[3 * r2], &rec.L[3 * r2]);
+          rec.G[r2] = (float)(P.M[3 * r2] * d[0] + P.M[3 * r2 + 1] * d[1] + P.M[3 * r2 + 2] * d[2]);
+        }
+        rec.a = (float)(2.0 / P.e2);
+        rec.b = (float)(P.e2 / P.e1);
+        rec.c = (float)(2.0 / P.e1);
+        // F >= max(|x'|)^(2/e1): cull when max|x'| > kFCut^(e1/2) (+0.1% margin)
+        rec.mcut = __double2float_ru(pow((double)kFCut, 0.5 * P.e1) * 1.001);
+        rec.cx = (float)cref[0];
+        rec.cy = (float)cref[1];
+        rec.cz = (float)cref[2];
+        rec.sigma = (float)P.sigma;
+        // class weights: logits (logit-sum) or softmax (prob-sum)
+        if (A.cfg.semantic_mode == 1) {
+          double m = logits[0];
+          for (int k = 1; k < C; ++k) m = fmax(m, logits[k]);
+          double s = 0.0;
+          for (int k = 0; k < C; ++k) s += exp(logits[k] - m);
+          for (int k = 0; k < C; ++k) lrow[k] = (float)(exp(logits[k] - m) / s);
+        } else {
+          for (int k = 0; k < C; ++k) lrow[k] = (float)logits[k];
+        }
+        lrow[A.cm] = (float)P.sigma;
+      }
+    }
+  }
+  reinterpret_cast<PrimRec*>(A.recs)[gi] = rec;
+  A.counts[gi] = count;
+  int* win = A.windows + 6 * gi;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    win[k] = rec.lo[k];
+    win[3 + k] = rec.hi[k];
+  }
+}
+
+// K3: one thread per primitive; entries in (tz, ty, tx) order, primitive
+// order preserved by the prefix offsets, so the stable radix sort by key
+// yields ascending primitive ids per tile (the oracle's bins).
+__global__ void emit_kernel(EmitArgs A) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t FN = (int64_t)A.n_frames * A.n_prims;
+  if (gi >= FN) return;
+  const int cnt = A.counts[gi];
+  if (cnt == 0) return;
+  const int f = (int)(gi / A.n_prims);
+  const int i = (int)(gi - (int64_t)f * A.n_prims);
+  const int* w = A.windows + 6 * gi;
+  int64_t o = A.offs[gi];
+  const uint32_t base = (uint32_t)f * (uint32_t)A.tiles_per_frame;
+  for (int tz = w[2] / kTileZ; tz <= w[5] / kTileZ; ++tz)
+    for (int ty = w[1] / kTileY; ty <= w[4] / kTileY; ++ty)
+      for (int tx = w[0] / kTileX; tx <= w[3] / kTileX; ++tx) {
+        const uint32_t key = base + (uint32_t)(tx + A.ntx * (ty + A.nty * tz));
+        A.keys[o] = key;
+        A.vals[o] = i;
+        ++o;
+        atomicAdd(A.tile_cnt + key, 1);
+      }
+}
+
+}  // namespace sqv

@@ -1,0 +1,341 @@
+"""The voxelize module of SPEC.md:317-400, on B200 kernels.
+
+Drop-in operations (same names, arguments and meaning as the SPEC):
+
+- ``voxelize(scene, spec, cfg) -> (SemanticGrid, DenseGrids)``
+- ``voxelize_bruteforce(scene, spec, cfg) -> (SemanticGrid, DenseGrids)`` SPEC.md:355-363
+- ``finalize(dense, tau, classes) -> SemanticGrid``
+- types ``VoxelGridSpec`` / ``VoxelizeConfig`` / ``DenseGrids`` / ``SemanticGrid``
+  
+
+plus the throughput entry the scene-per-call API cannot provide:
+
+- ``Voxelizer(spec, cfg, n_classes)(batch)`` — F frames of N primitives
+  (``PrimitiveBatch``, FP64 SoA on host or device) in one call, outputs left
+  on the device as torch tensors.
+
+Everything runs in libsqv.so (include/sqv.h ``sqv_voxelize``): prep ->
+scan -> emit -> radix sort -> evaluate+finalize.  There is no CPU path.
+
+Layout: voxel arrays are x-fastest.  Device tensors are
+``labels[F, nz, ny, nx]`` (uint8), ``v_o[F, nz, ny, nx]``,
+``v_c[F, nz, ny, nx, C]`` (float32, SPEC.md:113 allows FP32 storage).  The
+drop-in grids expose the SPEC's logical (nx, ny, nz) indexing as
+transposed NumPy views of that memory.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _lib
+from .core import ClassTable, PrimitiveBatch, Scene, bad_bits_message
+
+SEMANTIC_MODES = ("logit-sum", "prob-sum")
+
+
+@dataclass(frozen=True)
+class VoxelGridSpec:
+    """origin (min corner, m), dims (nx, ny, nz), resolution (m).  Occ3D default
+    (SPEC.md:326): (-40, -40, -1), (200, 200, 16), 0.4."""
+
+    origin: tuple = (-40.0, -40.0, -1.0)
+    dims: tuple = (200, 200, 16)
+    resolution: float = 0.4
+
+    def __post_init__(self):
+        origin = tuple(float(v) for v in self.origin)
+        dims = tuple(int(v) for v in self.dims)
+        if len(origin) != 3 or len(dims) != 3:
+            raise ValueError("origin and dims must have 3 components")
+        if not all(np.isfinite(origin)):
+            raise ValueError("origin must be finite")
+        if any(d < 1 for d in dims):
+            raise ValueError("dims must be >= 1 each")
+        if not (float(self.resolution) > 0.0 and np.isfinite(float(self.resolution))):
+            raise ValueError("resolution must be > 0")
+        object.__setattr__(self, "origin", origin)
+        object.__setattr__(self, "dims", dims)
+        object.__setattr__(self, "resolution", float(self.resolution))
+
+    @property
+    def n_voxels(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    def _c(self) -> _lib.Grid:
+        g = _lib.Grid()
+        g.origin[:] = self.origin
+        g.dims[:] = self.dims
+        g.resolution = self.resolution
+        return g
+
+
+@dataclass(frozen=True)
+class VoxelizeConfig:
+    """tau (default 0.01), neighborhood_radius (voxels, default 5),
+    semantic_mode ("logit-sum" | "prob-sum").  window_extent is the ledger's
+    max-K expansion factor (default 2.5)."""
+
+    tau: float = 0.01
+    neighborhood_radius: int = 5
+    semantic_mode: str = "logit-sum"
+    window_extent: float = 2.5
+
+    def __post_init__(self):
+        if not (float(self.tau) >= 0.0):
+            raise ValueError("tau must be >= 0")
+        if int(self.neighborhood_radius) != self.neighborhood_radius or self.neighborhood_radius < 0:
+            raise ValueError("neighborhood_radius must be a non-negative integer")
+        if self.semantic_mode not in SEMANTIC_MODES:
+            raise ValueError(f"semantic_mode must be one of {SEMANTIC_MODES}")
+        if not (float(self.window_extent) >= 0.0 and np.isfinite(float(self.window_extent))):
+            raise ValueError("window_extent must be finite and >= 0")
+
+
+@dataclass
+class DenseGrids:
+    """v_o (nx, ny, nz) >= 0 and v_c (nx, ny, nz, C)."""
+
+    v_o: Any
+    v_c: Any
+
+
+@dataclass
+class SemanticGrid:
+    """labels (nx, ny, nz): class id in [0, C) or classes.free_index."""
+
+    labels: Any
+    spec: VoxelGridSpec
+    classes: ClassTable
+
+
+@dataclass
+class VoxelizeResult:
+    """Device outputs of one batched call (torch tensors, x-fastest memory)."""
+
+    labels: Any                 # uint8 [F, nz, ny, nx]; free voxels = free_code
+    v_o: Any = None             # float32 [F, nz, ny, nx]
+    v_c: Any = None             # float32 [F, nz, ny, nx, C]
+    free_code: int = 255
+    n_pairs: int = 0            # algorithmic (primitive, in-window voxel) pairs
+    n_entries: int = 0          # (tile, primitive) bin entries
+    bins: dict | None = None    # windows / tile_off / prim_ids when requested
+
+
+def free_code_for(free_index: int, n_classes: int) -> int:
+    """The u8 label written for free voxels: free_index itself when it fits a
+    byte, else 255 (remapped on the host by ``SemanticGrid`` construction)."""
+    if 0 <= free_index <= 255 and free_index >= n_classes:
+        return int(free_index)
+    return 255
+
+
+class Voxelizer:
+    """Reusable B200 voxelizer for one grid/config/class count.
+
+    Holds the device workspace (grown on demand, torch caching allocator) and
+    runs ``sqv_voxelize`` on the current CUDA stream.
+    """
+
+    def __init__(self, spec: VoxelGridSpec = VoxelGridSpec(), cfg: VoxelizeConfig = VoxelizeConfig(),
+                 n_classes: int = 18, free_index: int | None = None, *, truncate: bool = True,
+                 device=None):
+        import torch
+        self.torch = torch
+        self.device = _lib.require_cuda(device)
+        self.L = _lib.lib()
+        if not (1 <= n_classes <= _lib.MAX_CLASSES):
+            raise ValueError(f"n_classes must lie in [1, {_lib.MAX_CLASSES}] on the device path")
+        self.spec, self.cfg, self.C = spec, cfg, int(n_classes)
+        self.free_index = self.C if free_index is None else int(free_index)
+        if 0 <= self.free_index < self.C:
+            raise ValueError("free_index must lie outside [0, C)")
+        self.free_code = free_code_for(self.free_index, self.C)
+        self.truncate = bool(truncate)
+        self._grid = spec._c()
+        c = _lib.Cfg()
+        c.tau = float(cfg.tau)
+        c.neighborhood_radius = int(cfg.neighborhood_radius)
+        c.truncate = int(self.truncate)
+        c.semantic_mode = SEMANTIC_MODES.index(cfg.semantic_mode)
+        c.free_label = self.free_code
+        c.window_extent = float(cfg.window_extent)
+        self._cfg = c
+        self._ws = None
+        self.tiles_per_frame = int(self.L.sqv_tiles_per_frame(ctypes.byref(self._grid)))
+
+    # ---- inputs -----------------------------------------------------------
+    def _dev(self, a, dtype):
+        t = self.torch
+        if isinstance(a, np.ndarray):
+            a = t.from_numpy(np.ascontiguousarray(a))
+        a = a.to(device=self.device, dtype=dtype, non_blocking=True)
+        return a.contiguous()
+
+    def to_device(self, batch: PrimitiveBatch) -> PrimitiveBatch:
+        t = self.torch
+        f = [self._dev(getattr(batch, k), t.float64) for k in PrimitiveBatch.FIELDS]
+        nv = None if batch.n_valid is None else self._dev(batch.n_valid, t.int32)
+        return PrimitiveBatch(*f, n_valid=nv)
+
+    def _workspace(self, nbytes: int):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = self.torch.empty(int(nbytes * 1.25) + 4096, dtype=self.torch.uint8,
+                                        device=self.device)
+        return self._ws
+
+    # ---- run ----------------------------------------------------------------
+    def alloc(self, n_frames: int, dense: bool = True) -> VoxelizeResult:
+        t = self.torch
+        nx, ny, nz = self.spec.dims
+        out = VoxelizeResult(labels=t.empty((n_frames, nz, ny, nx), dtype=t.uint8,
+                                            device=self.device), free_code=self.free_code)
+        if dense:
+            out.v_o = t.empty((n_frames, nz, ny, nx), dtype=t.float32, device=self.device)
+            out.v_c = t.empty((n_frames, nz, ny, nx, self.C), dtype=t.float32, device=self.device)
+        return out
+
+    def __call__(self, batch: PrimitiveBatch, *, dense: bool = True, bins: bool = False,
+                 out: VoxelizeResult | None = None) -> VoxelizeResult:
+        """Voxelize F frames.  Host inputs are copied to the device first
+        (non_blocking from pinned memory).  ``out`` may be preallocated with
+        ``alloc``; ``dense=False`` keeps v_o/v_c on chip (labels only)."""
+        t = self.torch
+        if batch.n_classes != self.C:
+            raise ValueError(f"batch has {batch.n_classes} classes, voxelizer expects {self.C}")
+        db = self.to_device(batch)
+        F, N = db.n_frames, db.n_prims
+        if out is None:
+            out = self.alloc(F, dense)
+        out.free_code = self.free_code
+        P = _lib.Prims()
+        P.mu, P.scale, P.rot = db.mu.data_ptr(), db.scale.data_ptr(), db.rot.data_ptr()
+        P.opacity, P.eps, P.logits = db.opacity.data_ptr(), db.eps.data_ptr(), db.logits.data_ptr()
+        P.n_valid = None if db.n_valid is None else db.n_valid.data_ptr()
+        P.n_frames, P.n_prims, P.n_classes = F, N, self.C
+        O = _lib.Outputs()
+        O.labels = out.labels.data_ptr()
+        O.v_o = out.v_o.data_ptr() if out.v_o is not None else None
+        O.v_c = out.v_c.data_ptr() if out.v_c is not None else None
+        B = _lib.Bins()
+        bins_t = None
+        if bins:
+            T = self.tiles_per_frame
+            bins_t = {"windows": t.empty((F, N, 6), dtype=t.int32, device=self.device),
+                      "tile_off": t.empty(F * T + 1, dtype=t.int32, device=self.device),
+                      "prim_ids": t.empty(1, dtype=t.int32, device=self.device)}
+            B.windows = bins_t["windows"].data_ptr()
+            B.tile_off = bins_t["tile_off"].data_ptr()
+        stream = _lib.stream_ptr(self.device)
+        need = ctypes.c_size_t(0)
+        bad_prim = ctypes.c_int64(-1)
+        bad_bits = ctypes.c_int32(0)
+        ws_bytes = int(self.L.sqv_workspace_bytes(F, N, self.C, ctypes.byref(self._grid), 0))
+        for _attempt in range(4):
+            ws = self._workspace(ws_bytes)
+            if bins:
+                B.prim_ids = bins_t["prim_ids"].data_ptr()
+                B.capacity = bins_t["prim_ids"].numel()
+            rc = self.L.sqv_voxelize(ctypes.byref(P), ctypes.byref(self._grid),
+                                     ctypes.byref(self._cfg), ctypes.byref(O), ctypes.byref(B),
+                                     ws.data_ptr(), ws.numel(), ctypes.byref(need),
+                                     ctypes.byref(bad_prim), ctypes.byref(bad_bits), stream)
+            if rc == _lib.SQV_ERR_WORKSPACE:
+                ws_bytes = int(need.value)
+                continue
+            if rc == _lib.SQV_ERR_CAPACITY and bins:
+                bins_t["prim_ids"] = t.empty(max(1, int(B.n_entries)), dtype=t.int32,
+                                             device=self.device)
+                continue
+            if rc == _lib.SQV_ERR_INVALID_PRIM:
+                f, i = divmod(int(bad_prim.value), max(N, 1))
+                raise ValueError(f"frame {f} primitive {i}: "
+                                 f"{bad_bits_message(int(bad_bits.value))}")
+            _lib.check(rc, "sqv_voxelize")
+            break
+        else:
+            raise RuntimeError("sqv_voxelize: workspace negotiation did not converge")
+        out.n_pairs, out.n_entries = int(B.n_pairs), int(B.n_entries)
+        if bins:
+            bins_t["prim_ids"] = bins_t["prim_ids"][: out.n_entries]
+            out.bins = bins_t
+        return out
+
+
+# ---- conversions to the SPEC's host types ---------------------------------
+
+def _logical(a: np.ndarray) -> np.ndarray:
+    """(nz, ny, nx[, C]) x-fastest memory -> (nx, ny, nz[, C]) view."""
+    return a.transpose(2, 1, 0, 3) if a.ndim == 4 else a.transpose(2, 1, 0)
+
+
+def labels_to_host(labels_u8: np.ndarray, free_code: int, free_index: int) -> np.ndarray:
+    if free_code == free_index:
+        return labels_u8
+    out = labels_u8.astype(np.int64)
+    out[labels_u8 == free_code] = free_index
+    return out
+
+
+def _as_batch(scene) -> tuple[PrimitiveBatch, ClassTable]:
+    if isinstance(scene, PrimitiveBatch):
+        return scene, ClassTable.numbered(scene.n_classes)
+    if hasattr(scene, "primitives") and hasattr(scene, "classes"):
+        return PrimitiveBatch.from_scene(scene), scene.classes
+    raise TypeError("scene must be a Scene (sqocc.core or ours) or a PrimitiveBatch")
+
+
+def _run_scene(scene, spec, cfg, truncate):
+    batch, classes = _as_batch(scene)
+    if batch.n_frames != 1:
+        raise ValueError("voxelize() takes one scene; use Voxelizer for batches")
+    vox = Voxelizer(spec, cfg, len(classes), classes.free_index, truncate=truncate)
+    r = vox(batch, dense=True)
+    lab = r.labels[0].cpu().numpy()
+    v_o = r.v_o[0].cpu().numpy()
+    v_c = r.v_c[0].cpu().numpy()
+    lab = labels_to_host(lab, r.free_code, classes.free_index)
+    return (SemanticGrid(_logical(lab), spec, classes), DenseGrids(_logical(v_o), _logical(v_c)))
+
+
+def voxelize(scene, spec: VoxelGridSpec = VoxelGridSpec(),
+             cfg: VoxelizeConfig = VoxelizeConfig()) -> tuple[SemanticGrid, DenseGrids]:
+    """Eqs. 8-9 with the truncated window, then finalize."""
+    return _run_scene(scene, spec, cfg, truncate=True)
+
+
+def voxelize_bruteforce(scene, spec: VoxelGridSpec = VoxelGridSpec(),
+                        cfg: VoxelizeConfig = VoxelizeConfig()) -> tuple[SemanticGrid, DenseGrids]:
+    """Untruncated gather: every primitive over the whole
+    grid, same sigma = 0 skip and finalize as voxelize."""
+    return _run_scene(scene, spec, cfg, truncate=False)
+
+
+def finalize(dense: DenseGrids, tau: float, classes: ClassTable) -> SemanticGrid:
+    """Labels from dense grids — the device finalize kernel."""
+    import torch
+    dev = _lib.require_cuda()
+    L = _lib.lib()
+    if not (float(tau) >= 0.0):
+        raise ValueError("tau must be >= 0")
+    C = len(classes)
+    v_o = np.asarray(dense.v_o)
+    v_c = np.asarray(dense.v_c)
+    if v_c.shape[:-1] != v_o.shape or v_c.shape[-1] != C:
+        raise ValueError("dense grids and classes are inconsistent")
+    shape = v_o.shape
+    # memory order of the logical (nx, ny, nz) view: x-fastest -> C order of (nz, ny, nx)
+    vo_mem = np.ascontiguousarray(v_o.transpose(2, 1, 0), np.float32)
+    vc_mem = np.ascontiguousarray(v_c.transpose(2, 1, 0, 3), np.float32)
+    t_vo = torch.from_numpy(vo_mem).to(dev)
+    t_vc = torch.from_numpy(vc_mem).to(dev)
+    code = free_code_for(classes.free_index, C)
+    lab = torch.empty(vo_mem.shape, dtype=torch.uint8, device=dev)
+    _lib.check(L.sqv_finalize(t_vo.data_ptr(), t_vc.data_ptr(), vo_mem.size, C, float(tau), code,
+                              lab.data_ptr(), _lib.stream_ptr(dev)), "sqv_finalize")
+    lab_h = labels_to_host(lab.cpu().numpy(), code, classes.free_index)
+    spec = VoxelGridSpec(dims=shape)
+    return SemanticGrid(_logical(lab_h), spec, classes)

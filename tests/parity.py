@@ -1,0 +1,68 @@
+"""Parity criteria between the B200 path and the FP64 oracle (north_star):
+
+* bins, windows, pair counts and confusion counts: bit-exact;
+* densities: |v_o - ref| <= VO_REL * max(ref, VO_FLOOR)  (1e-5 relative, with
+  a floor of 1e-3*tau below which "relative" is meaningless: the FP32
+  evaluation of exp(-F) has an F-proportional error);
+* labels: a voxel may disagree only where the oracle's top-2 class scores
+  differ by < LABEL_GAP * max(1, |top-1|), or where the oracle's v_o lies
+  within VO_REL of tau (a tau flip); overall agreement >= 99.99%.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+VO_REL = 1e-5
+VO_FLOOR_FRAC_TAU = 1e-3
+LABEL_GAP = 1e-5
+MIN_AGREEMENT = 0.9999
+
+
+def vo_check(gpu, ref, tau, rel=VO_REL, floor=None):
+    gpu = np.asarray(gpu, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    if floor is None:
+        floor = max(VO_FLOOR_FRAC_TAU * tau, 1e-7)
+    err = np.abs(gpu - ref)
+    bound = rel * np.maximum(ref, floor)
+    bad = err > bound
+    worst = float(np.max(err / np.maximum(ref, floor))) if err.size else 0.0
+    return {"n_bad": int(bad.sum()), "worst_rel": worst, "bad_idx": np.flatnonzero(bad)[:10]}
+
+
+def label_check(gpu_lab, ref_lab, ref_vo, ref_vc, tau, free_code):
+    g = np.asarray(gpu_lab).ravel()
+    r = np.asarray(ref_lab).ravel()
+    vo = np.asarray(ref_vo, np.float64).ravel()
+    C = ref_vc.shape[-1]
+    vc = np.asarray(ref_vc, np.float64).reshape(-1, C)
+    mism = np.flatnonzero(g != r)
+    unexplained = []
+    for v in mism:
+        if abs(vo[v] - tau) <= VO_REL * max(tau, VO_FLOOR_FRAC_TAU * tau, 1e-30):
+            continue  # tau flip
+        if g[v] != free_code and r[v] != free_code:
+            top = vc[v, r[v]]
+            if top - vc[v, g[v]] <= LABEL_GAP * max(1.0, abs(top)):
+                continue  # near-tie in the oracle's scores
+        unexplained.append(int(v))
+    agree = 1.0 - mism.size / max(g.size, 1)
+    return {"n_mismatch": int(mism.size), "unexplained": unexplained[:10],
+            "n_unexplained": len(unexplained), "agreement": agree}
+
+
+def assert_parity(gpu, ref, tau, free_code, check_vc=True):
+    """gpu/ref: dicts with v_o [F,V], v_c [F,V,C] (ref FP64), labels [F,V]."""
+    vo = vo_check(gpu["v_o"], ref["v_o"], tau)
+    assert vo["n_bad"] == 0, f"v_o out of tolerance: {vo}"
+    lab = label_check(gpu["labels"], ref["labels"], ref["v_o"], ref["v_c"], tau, free_code)
+    assert lab["n_unexplained"] == 0, f"unexplained label mismatches: {lab}"
+    assert lab["agreement"] >= MIN_AGREEMENT, lab
+    if check_vc:
+        # class weights: absolute error relative to the voxel's weight scale
+        vc_g = np.asarray(gpu["v_c"], np.float64)
+        vc_r = np.asarray(ref["v_c"], np.float64)
+        scale = np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), 1e-3)
+        rel = np.abs(vc_g - vc_r) / scale
+        assert float(rel.max(initial=0.0)) <= 1e-4, f"v_c worst {float(rel.max())}"
+    return vo, lab

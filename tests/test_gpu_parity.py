@@ -1,0 +1,288 @@
+"""B200 path vs the FP64 oracle / the reference's golden vectors (-m gpu).
+
+Every call goes through libsqv.so (include/sqv.h) via the package's public
+API; the oracle (oracle/) is only the checker.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from oracle import oracle as O
+from parity import assert_parity, label_check, vo_check
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2511_17361_b200 as P
+    return P
+
+
+def _batch_from(g):
+    P = _pkg()
+    return P.PrimitiveBatch(*(np.asarray(g[k])[None] for k in
+                              ("mu", "scale", "rot", "opacity", "eps", "logits")))
+
+
+def _run(batch, spec, cfg, C, free=None, truncate=True, bins=False):
+    P = _pkg()
+    vox = P.Voxelizer(spec, cfg, C, free, truncate=truncate)
+    r = vox(batch, dense=True, bins=bins)
+    F = batch.n_frames
+    out = {"labels": r.labels.reshape(F, -1).cpu().numpy(),
+           "v_o": r.v_o.reshape(F, -1).cpu().numpy(),
+           "v_c": r.v_c.reshape(F, spec.n_voxels, C).cpu().numpy(),
+           "n_pairs": r.n_pairs, "free_code": r.free_code}
+    if bins:
+        out["windows"] = r.bins["windows"].cpu().numpy()
+        out["tile_off"] = r.bins["tile_off"].cpu().numpy()
+        out["prim_ids"] = r.bins["prim_ids"].cpu().numpy()
+    return out
+
+
+def _oracle(batch, spec, cfg, free_code, truncate=True):
+    p = O.Prims.of(batch)
+    grid = O.Grid(spec.origin, spec.dims, spec.resolution)
+    c = O.Cfg(cfg.tau, cfg.neighborhood_radius, truncate, cfg.semantic_mode == "prob-sum",
+              free_code, cfg.window_extent)
+    r = O.voxelize(p, grid, c)
+    r["windows"] = O.prep(p, grid, c)
+    return r, grid
+
+
+# ---- point-wise math vs the reference's sqocc.core ------------------------
+
+def test_density_pairs_vs_reference_core():
+    from paper_2511_17361_b200.density import density_pairs
+    g = load_golden("core_pairs.npz")
+    F, d = density_pairs(_batch_from(g), g["points"], g["pair_prim"])
+    Fr, dr = g["F"], g["density"]
+    live = Fr < 80
+    relF = np.abs(F[live] - Fr[live]) / np.maximum(Fr[live], 1e-3)
+    assert relF.max() < 2e-5, relF.max()
+    # exp(-F): error ~ |dF|; relative 1e-5 where the density is >= 1e-3
+    big = dr >= 1e-3
+    assert np.max(np.abs(d[big] - dr[big]) / dr[big]) < 1e-5
+    assert np.all(np.abs(d - dr) <= 1e-5 * np.maximum(dr, 1e-3) + 1e-38)
+
+
+# ---- reference golden scenes ------------------------------------------------
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "voxelize_*.npz"))),
+                         ids=lambda p: os.path.basename(p)[9:-4])
+def test_golden_scenes(path):
+    P = _pkg()
+    g = dict(np.load(path))
+    C = g["logits"].shape[1]
+    spec = P.VoxelGridSpec(tuple(g["origin"]), tuple(int(x) for x in g["dims"]), float(g["res"]))
+    cfg = P.VoxelizeConfig(float(g["tau"]), int(g["radius"]),
+                           "prob-sum" if bool(g["prob_sum"]) else "logit-sum")
+    out = _run(_batch_from(g), spec, cfg, C, int(g["free_label"]), truncate=bool(g["truncate"]),
+               bins=True)
+    np.testing.assert_array_equal(out["windows"][0], g["windows"])
+    np.testing.assert_array_equal(out["tile_off"], g["tile_off"])
+    np.testing.assert_array_equal(out["prim_ids"], g["prim_ids"])
+    assert out["n_pairs"] == int(g["n_pairs"])
+    ref = {"v_o": g["v_o"][None], "v_c": g["v_c"][None], "labels": g["labels"][None]}
+    assert_parity(out, ref, float(g["tau"]), int(g["free_label"]))
+
+
+# ---- seeded scenes vs the oracle ----------------------------------------------
+
+def _scene(seed, n, C=18, **kw):
+    from paper_2511_17361_b200.scenegen import gen_frames
+    return gen_frames(seed, kw.pop("frames", 1), n, C, **kw)
+
+
+def test_config1_occ3d_256():
+    """Config 1: 256 SQs on the Occ3D grid, full parity + exact bins."""
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    b = _scene(11, 256)
+    out = _run(b, spec, cfg, 18, bins=True)
+    ref, grid = _oracle(b, spec, cfg, out["free_code"])
+    np.testing.assert_array_equal(out["windows"], ref["windows"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert out["n_pairs"] == ref["n_pairs"]
+    vo, lab = assert_parity(out, ref, cfg.tau, out["free_code"])
+    print("config1 worst v_o rel", vo["worst_rel"], "label agreement", lab["agreement"])
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_acceptance4_bruteforce_equivalence(seed):
+    """SPEC.md:630 #4: <=50 prims, 32^3: untruncated voxelize == bruteforce oracle."""
+    P = _pkg()
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 51))
+    spec = P.VoxelGridSpec((-6.4, -6.4, -6.4), (32, 32, 32), 0.4)
+    cfg = P.VoxelizeConfig()
+    b = _scene(500 + seed, n, C=8, origin=spec.origin, dims=spec.dims,
+               resolution=spec.resolution, smax=2.0)
+    out = _run(b, spec, cfg, 8, truncate=False)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"], truncate=False)
+    assert out["n_pairs"] == ref["n_pairs"]
+    assert_parity(out, ref, cfg.tau, out["free_code"])
+    # the truncated window misses only tail mass: mismatch rate < 0.5%
+    tr = _run(b, spec, cfg, 8, truncate=True)
+    assert np.mean(tr["labels"] != out["labels"]) < 0.005
+
+
+@pytest.mark.parametrize("kw", [dict(emin=0.1), dict(smax=1.0), dict(smin=0.05, smax=0.6)],
+                         ids=["stress_eps", "sparse", "needles"])
+def test_stress_sets(kw):
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    b = _scene(21, 600, **kw)
+    out = _run(b, spec, cfg, 18)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"])
+    assert_parity(out, ref, cfg.tau, out["free_code"])
+
+
+def test_prob_sum_and_ragged_batch_determinism():
+    """prob-sum mode; ragged frames (n_valid); a frame's output does not depend
+    on its batch position (bit-identical)."""
+    P = _pkg()
+    spec = P.VoxelGridSpec((-8.0, -8.0, -2.0), (40, 40, 16), 0.4)
+    cfg = P.VoxelizeConfig(semantic_mode="prob-sum")
+    b = _scene(31, 120, C=5, frames=3, origin=spec.origin, dims=spec.dims, smax=2.0)
+    b.n_valid = np.array([120, 37, 0], np.int32)
+    out = _run(b, spec, cfg, 5)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"])
+    assert_parity(out, ref, cfg.tau, out["free_code"])
+    assert np.all(out["labels"][2] == out["free_code"]) and np.all(out["v_o"][2] == 0)
+    single = _run(b.frames(1, 2), spec, cfg, 5)
+    assert np.array_equal(single["v_o"][0], out["v_o"][1])
+    assert np.array_equal(single["v_c"][0], out["v_c"][1])
+    again = _run(b, spec, cfg, 5)
+    assert all(np.array_equal(again[k], out[k]) for k in ("labels", "v_o", "v_c"))
+
+
+def test_config2_frame_large_properties():
+    """One config-2 frame (2k SQs): bins exact, pair count exact, >= 99.99% label
+    agreement, v_o within tolerance."""
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    b = _scene(7, 2000)
+    out = _run(b, spec, cfg, 18, bins=True)
+    ref, grid = _oracle(b, spec, cfg, out["free_code"])
+    np.testing.assert_array_equal(out["windows"], ref["windows"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert out["n_pairs"] == ref["n_pairs"]
+    vo, lab = assert_parity(out, ref, cfg.tau, out["free_code"])
+    print("config2 pairs", ref["n_pairs"], "worst v_o rel", vo["worst_rel"], "agreement",
+          lab["agreement"])
+
+
+def test_fine_grid_config4_slice():
+    """Config 4 geometry (400x400x32 @0.2) with a reduced primitive count."""
+    P = _pkg()
+    spec = P.VoxelGridSpec((-40.0, -40.0, -1.0), (400, 400, 32), 0.2)
+    cfg = P.VoxelizeConfig()
+    b = _scene(9, 300, origin=spec.origin, dims=spec.dims, resolution=spec.resolution)
+    out = _run(b, spec, cfg, 18, bins=True)
+    ref, grid = _oracle(b, spec, cfg, out["free_code"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert_parity(out, ref, cfg.tau, out["free_code"])
+
+
+# ---- drop-in API ----------------------------------------------------------------
+
+def test_dropin_scene_api_and_spec_examples():
+    P = _pkg()
+    classes = P.ClassTable(("a",))
+    spec = P.VoxelGridSpec((-2.0, -2.0, -2.0), (8, 8, 8), 0.5)
+    # SPEC.md:351 empty scene -> all free, v_o == 0
+    sem, dense = P.voxelize(P.Scene([], classes), spec)
+    assert np.all(sem.labels == classes.free_index) and np.all(dense.v_o == 0)
+    # SPEC.md:352 unit sphere on a voxel centre, C=1 -> v_o = 1 there, class 0
+    sq = P.SuperQuadric(mu=[0.25, 0.25, 0.25], scale=[1, 1, 1], rot=[1, 0, 0, 0], opacity=1.0,
+                        logits=[0.3], eps1=1.0, eps2=1.0)
+    sem, dense = P.voxelize(P.Scene([sq], classes), spec)
+    assert dense.v_o.shape == (8, 8, 8) and dense.v_c.shape == (8, 8, 8, 1)
+    assert abs(dense.v_o[4, 4, 4] - 1.0) < 1e-6 and sem.labels[4, 4, 4] == 0
+    # finalize: tau = 0 -> no free voxel where anything contributed; tau = inf -> all free
+    assert np.all(P.finalize(dense, 0.0, classes).labels[dense.v_o > 0] == 0)
+    assert np.all(P.finalize(dense, float("inf"), classes).labels == classes.free_index)
+    # tau sweep monotonicity
+    occ = [int(np.sum(P.finalize(dense, t, classes).labels != classes.free_index))
+           for t in (0.005, 0.01, 0.02)]
+    assert occ[0] >= occ[1] >= occ[2]
+
+
+def test_sigma_scaling_argmax_invariance():
+    """scaling all sigma leaves labels unchanged where occupied."""
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    b = _scene(41, 300, smax=1.5)
+    b2 = P.PrimitiveBatch(b.mu, b.scale, b.rot, b.opacity * 0.5, b.eps, b.logits)
+    o1 = _run(b, spec, cfg, 18)
+    o2 = _run(b2, spec, cfg, 18)
+    both = (o1["labels"] != o1["free_code"]) & (o2["labels"] != o2["free_code"])
+    assert np.mean(o1["labels"][both] == o2["labels"][both]) > 0.9999
+
+
+def test_invalid_primitive_messages():
+    P = _pkg()
+    spec = P.VoxelGridSpec((-2.0, -2.0, -2.0), (8, 8, 8), 0.5)
+    vox = P.Voxelizer(spec, P.VoxelizeConfig(), 2)
+    base = _scene(3, 4, C=2, origin=spec.origin, dims=spec.dims, resolution=spec.resolution)
+    cases = [("scale", (0, 1, 2), -1.0, "scale components must be strictly positive"),
+             ("opacity", (0, 2), 1.5, "opacity must lie in [0, 1]"),
+             ("mu", (0, 3, 0), np.nan, "mu/scale must be finite"),
+             ("logits", (0, 0, 1), np.inf, "logits must be finite")]
+    for field, idx, val, msg in cases:
+        arrs = {k: np.array(getattr(base, k)) for k in P.PrimitiveBatch.FIELDS}
+        arrs[field][idx] = val
+        with pytest.raises(ValueError, match=msg):
+            vox(P.PrimitiveBatch(**arrs))
+    arrs = {k: np.array(getattr(base, k)) for k in P.PrimitiveBatch.FIELDS}
+    arrs["rot"][0, 1] = 0.0
+    with pytest.raises(ValueError, match="near-zero quaternion"):
+        vox(P.PrimitiveBatch(**arrs))
+
+
+# ---- metrics ---------------------------------------------------------------------
+
+def test_confusion_kernel_vs_golden():
+    from paper_2511_17361_b200.metrics import confusion_matrix
+    g = load_golden("confusion.npz")
+    s = c0 = 0
+    for n, C in zip(g["lens"], g["C"]):
+        k = (C + 1) ** 2
+        cm = confusion_matrix(g["pred"][s:s + n], g["gt"][s:s + n], int(C)).cpu().numpy()
+        np.testing.assert_array_equal(cm.ravel(), g["cm"][c0:c0 + k])
+        s += n
+        c0 += k
+
+
+def test_confusion_large_and_iou_examples():
+    P = _pkg()
+    from paper_2511_17361_b200 import metrics as M
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 19, size=3_000_017).astype(np.uint8)
+    b = np.where(rng.uniform(size=a.size) < 0.7, a, rng.integers(0, 19, size=a.size)).astype(np.uint8)
+    a[a == 18] = 255
+    cm = M.confusion_matrix(a, b, 18).cpu().numpy()
+    np.testing.assert_array_equal(cm, O.confusion(a, b, 18))
+    # 2x2x1, pred {(0,0),(1,0)}, gt {(1,0),(1,1)} -> 1/3
+    classes = P.ClassTable(("x",))
+    spec = P.VoxelGridSpec(dims=(2, 2, 1))
+    pl = np.full((2, 2, 1), 1)
+    gl = np.full((2, 2, 1), 1)
+    pl[0, 0, 0] = pl[1, 0, 0] = 0
+    gl[1, 0, 0] = gl[1, 1, 0] = 0
+    pred = P.SemanticGrid(pl, spec, classes)
+    gt = P.SemanticGrid(gl, spec, classes)
+    assert abs(M.voxel_iou(pred, gt) - 1 / 3) < 1e-12
+    assert M.voxel_iou(pred, pred) == 1.0
+    per, m = M.miou(pred, pred)
+    assert m == 1.0
