@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sqv_kernels.cuh"
@@ -328,6 +329,10 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.nz = grid->dims[2];
   A.tau = tau_f32(cfg->tau);
   A.free_label = cfg->free_label;
+  {
+    const char* fe = std::getenv("SQV_FIELD");  // diagnostics only: 9 = reference 9-MUFU form
+    A.field = (fe && std::atoi(fe) == 9) ? 9 : 7;
+  }
   A.labels = out->labels;
   A.v_o = out->v_o;
   A.v_c = out->v_c;

@@ -1,22 +1,26 @@
 // sqv_eval.cu — K5: per-tile evaluator with fused finalize (the hot kernel).
 //
 // One CTA owns one 8x8x16 voxel tile of one frame (SQV_TILE_*) and gathers
-// the tile's primitive list (the bins, ascending primitive ids) in chunks
-// staged in shared memory.  Each of the 8 warps owns a 4x4x8 voxel block,
-// each lane a 1x1x4 z-column, so every (primitive, voxel) pair of the tile is
-// evaluated by exactly one thread and every voxel accumulates its
-// contributions in primitive order: the result is deterministic and does not
-// depend on the batch or the GPU count.
+// the tile's primitive list (the bins, ascending primitive ids), staged in
+// shared memory in chunks of up to kChunk primitives (one chunk for almost
+// every tile).  Each of the 8 warps owns a 4x4x8 voxel block, each lane a
+// 1x1x4 z-column, so every (primitive, voxel) pair of the tile is evaluated by
+// exactly one thread and every voxel accumulates its contributions in
+// primitive order: the result is deterministic and does not depend on the
+// batch or the GPU count.
+//
+// Per chunk each warp first builds a bitmask of the staged primitives whose
+// window meets its block (lane-parallel test + ballot), then walks only the
+// set bits, so a primitive that misses a warp costs that warp nothing.
 //
 // Per pair (core.py:237-282):
 //   x' = local coordinates / scale  — hi/lo split lattice stepping (exact
 //        offsets, no cancellation), see prep's split_row
-//   F  = (|x'0|^a + |x'1|^a)^b + |x'2|^c          — 8 MUFU (lg2/ex2)
+//   F  = (|x'0|^a + |x'1|^a)^b + |x'2|^c          — 7 MUFU (field_F7)
 //   w  = exp(-F) (0 for F >= kFCut)               — 1 MUFU
 //   v_o += sigma*w; v_c[k] += w*c_k               — C+1 FFMA, in registers
-// Culling (never changes an output bit, see kFCut): a warp skips a primitive
-// when its block misses the window, or when every live voxel has
-// max|x'| > mcut, i.e. F > kFCut.
+// Culling (never changes an output bit, see kFCut): skipped when every live
+// voxel of the warp has max|x'| > mcut, i.e. F > kFCut.
 // Epilogue = finalize: free if v_o < tau, else the first
 // argmax; dense grids and labels staged through shared memory and written
 // as coalesced row segments (x-fastest layout).
@@ -27,21 +31,26 @@ namespace sqv {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 64;  // primitives staged per chunk
-constexpr int kVPT = 4;     // voxels per thread (consecutive z)
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 256;            // primitives staged per chunk
+constexpr int kMaskWords = kChunk / 32;
+constexpr int kVPT = 4;                // voxels per thread (consecutive z)
 
 template <int CM>
 struct EvalShape {
   static constexpr int kLRow = (CM + 1 + 3) & ~3;  // class weights + sigma, float4-padded
-  static constexpr int kChunkBytes = kChunk * (kRecWords + kLRow) * 4;
+  static constexpr int kChunkBytes = kChunk * (kRecWords + kLRow) * 4 + kWarps * kMaskWords * 4;
+  static constexpr int kStageBytes = 512 * (CM * 4 + 4 + 1);
+  static constexpr int kSmem = kChunkBytes > kStageBytes ? kChunkBytes : kStageBytes;
 };
 
-template <int CM>
-__global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
+template <int CM, int FIELD>
+__global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(EvalArgs A) {
   using S = EvalShape<CM>;
   extern __shared__ __align__(16) float smem[];
-  float* s_rec = smem;                        // [kChunk][kRecWords]
-  float* s_lw = smem + kChunk * kRecWords;    // [kChunk][kLRow]
+  float* s_rec = smem;                                   // [kChunk][kRecWords]
+  float* s_lw = smem + kChunk * kRecWords;               // [kChunk][kLRow]
+  unsigned* s_mask = reinterpret_cast<unsigned*>(s_lw + kChunk * S::kLRow);  // [kWarps][kMaskWords]
 
   const int tile_g = blockIdx.x;
   const int f = tile_g / A.tiles_per_frame;
@@ -57,7 +66,6 @@ __global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
   const int x = bx0 + (lane & 3);
   const int y = by0 + ((lane >> 2) & 3);
   const int z0 = bz0 + (lane >> 4) * 4;
-  const float xf = (float)x, yf = (float)y, z0f = (float)z0;
 
   float acc[kVPT][CM + 1];
 #pragma unroll
@@ -66,8 +74,6 @@ __global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
     for (int k = 0; k <= CM; ++k) acc[v][k] = 0.0f;
 
   const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
-  const float* __restrict__ recs = A.recs;
-  const float* __restrict__ lrows = A.lrows;
   const int64_t fbase = (int64_t)f * A.n_prims;
 
   for (int c0 = beg; c0 < end; c0 += kChunk) {
@@ -78,67 +84,88 @@ __global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
       const int j = idx / (kRecWords / 4), q = idx - j * (kRecWords / 4);
       const int64_t g = fbase + A.prim_ids[c0 + j];
       reinterpret_cast<float4*>(s_rec)[idx] =
-          __ldg(reinterpret_cast<const float4*>(recs + g * kRecWords) + q);
+          __ldg(reinterpret_cast<const float4*>(A.recs + g * kRecWords) + q);
     }
     for (int idx = tid; idx < n * (S::kLRow / 4); idx += kThreads) {
       const int j = idx / (S::kLRow / 4), q = idx - j * (S::kLRow / 4);
       const int64_t g = fbase + A.prim_ids[c0 + j];
       reinterpret_cast<float4*>(s_lw)[idx] =
-          __ldg(reinterpret_cast<const float4*>(lrows + g * A.lrow) + q);
+          __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + q);
     }
     __syncthreads();
+    // per-warp hit masks: which staged primitives' windows meet this block
+    for (int q = 0; q * 32 < n; ++q) {
+      const int j = q * 32 + lane;
+      bool hit = false;
+      if (j < n) {
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        hit = !(bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
+                bz0 + 7 < R.lo[2] || bz0 > R.hi[2]);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_mask[warp * kMaskWords + q] = m;
+    }
+    __syncwarp();
 
-    for (int j = 0; j < n; ++j) {
-      const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
-      const int lox = R.lo[0], loy = R.lo[1], loz = R.lo[2];
-      const int hix = R.hi[0], hiy = R.hi[1], hiz = R.hi[2];
-      // warp-uniform: does this warp's 4x4x8 block meet the window?
-      if (bx0 + 3 < lox || bx0 > hix || by0 + 3 < loy || by0 > hiy || bz0 + 7 < loz ||
-          bz0 > hiz)
-        continue;
-      const bool in_xy = x >= lox && x <= hix && y >= loy && y <= hiy;
-      const float fx = xf - R.cx, fy = yf - R.cy, fz = z0f - R.cz;
-      // hi parts: exact; lo parts: small
-      float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
-      float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
-      float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
-      float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
-      float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
-      float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
-      const float mcut = R.mcut;
-      float p0[kVPT], p1[kVPT], p2[kVPT];
-      bool live[kVPT];
-      bool any = false;
+    for (int q = 0; q * 32 < n; ++q) {
+      unsigned m = s_mask[warp * kMaskWords + q];
+      while (m) {
+        const int j = q * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
+        const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
+        // hi parts: exact; lo parts: small
+        float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
+        float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
+        float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
+        float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
+        float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
+        float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
+        const float mcut = R.mcut;
+        const int loz = R.lo[2], hiz = R.hi[2];
+        float p0[kVPT], p1[kVPT], p2[kVPT];
+        bool live[kVPT];
+        bool any = false;
 #pragma unroll
-      for (int v = 0; v < kVPT; ++v) {
-        p0[v] = h0 + l0;
-        p1[v] = h1 + l1;
-        p2[v] = h2 + l2;
-        h0 += R.H[2];
-        h1 += R.H[5];
-        h2 += R.H[8];
-        l0 += R.L[2];
-        l1 += R.L[5];
-        l2 += R.L[8];
-        const int z = z0 + v;
-        const float m = fmaxf(fmaxf(fabsf(p0[v]), fabsf(p1[v])), fabsf(p2[v]));
-        live[v] = in_xy && z >= loz && z <= hiz && m <= mcut;
-        any |= live[v];
-      }
-      if (!__any_sync(0xffffffffu, any)) continue;
-      const float a = R.a, b = R.b, c = R.c;
-      float w[kVPT];
+        for (int v = 0; v < kVPT; ++v) {
+          p0[v] = h0 + l0;
+          p1[v] = h1 + l1;
+          p2[v] = h2 + l2;
+          h0 += R.H[2];
+          h1 += R.H[5];
+          h2 += R.H[8];
+          l0 += R.L[2];
+          l1 += R.L[5];
+          l2 += R.L[8];
+          const int z = z0 + v;
+          const float mm = fmaxf(fmaxf(fabsf(p0[v]), fabsf(p1[v])), fabsf(p2[v]));
+          live[v] = in_xy && z >= loz && z <= hiz && mm <= mcut;
+          any |= live[v];
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        const float a = R.a, b = R.b, c = R.c;
+        float w[kVPT];
 #pragma unroll
-      for (int v = 0; v < kVPT; ++v) {
-        const float F = field_F(p0[v], p1[v], p2[v], a, b, c);
-        w[v] = (live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;
-      }
-      const float* lw = s_lw + j * S::kLRow;
+        for (int v = 0; v < kVPT; ++v) {
+          const float F = FIELD == 7 ? field_F7(p0[v], p1[v], p2[v], a, b, c)
+                                     : field_F(p0[v], p1[v], p2[v], a, b, c);
+          w[v] = (live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;
+        }
+        const float4* lw = reinterpret_cast<const float4*>(s_lw + j * S::kLRow);
 #pragma unroll
-      for (int k = 0; k <= CM; ++k) {
-        const float ck = lw[k];
+        for (int k4 = 0; k4 < S::kLRow / 4; ++k4) {
+          const float4 c4 = lw[k4];
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-        for (int v = 0; v < kVPT; ++v) acc[v][k] = fmaf(w[v], ck, acc[v][k]);
+          for (int e = 0; e < 4; ++e) {
+            const int k = 4 * k4 + e;
+            if (k <= CM) {
+#pragma unroll
+              for (int v = 0; v < kVPT; ++v) acc[v][k] = fmaf(w[v], cc[e], acc[v][k]);
+            }
+          }
+        }
       }
     }
   }
@@ -187,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
     __syncthreads();
     const int xw = min(kTileX, nx - x_t);  // valid voxels per row
     // 64 rows (8 z x 8 y) of 8 voxels
-    for (int row = warp; row < 64; row += kThreads / 32) {
+    for (int row = warp; row < 64; row += kWarps) {
       const int yl = row & 7, zl = row >> 3;
       const int yy = y_t + yl, zz = zh + zl;
       if (yy >= ny || zz >= nz) continue;
@@ -207,14 +234,13 @@ __global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs A) {
 }
 
 template <int CM>
-int launch_cm(const EvalArgs& A, int n_tiles, cudaStream_t s) {
+int launch_cm(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = EvalShape<CM>;
-  const int stage_bytes = 512 * (CM * 4 + 4 + 1);
-  const int smem = S::kChunkBytes > stage_bytes ? S::kChunkBytes : stage_bytes;
-  if (cudaFuncSetAttribute(eval_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+  auto kern = field == 9 ? eval_kernel<CM, 9> : eval_kernel<CM, 7>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem) !=
       cudaSuccess)
     return check_launch("eval_kernel attribute");
-  eval_kernel<CM><<<n_tiles, kThreads, smem, s>>>(A);
+  kern<<<n_tiles, kThreads, S::kSmem, s>>>(A);
   count_launch();
   return check_launch("eval_kernel");
 }
@@ -236,15 +262,16 @@ int eval_cm_for(int C) {
 
 int eval_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return SQV_OK;
+  const int field = A.field == 9 ? 9 : 7;
   switch (cm) {
-    case 2: return launch_cm<2>(A, n_tiles, s);
-    case 4: return launch_cm<4>(A, n_tiles, s);
-    case 8: return launch_cm<8>(A, n_tiles, s);
-    case 12: return launch_cm<12>(A, n_tiles, s);
-    case 16: return launch_cm<16>(A, n_tiles, s);
-    case 18: return launch_cm<18>(A, n_tiles, s);
-    case 24: return launch_cm<24>(A, n_tiles, s);
-    case 32: return launch_cm<32>(A, n_tiles, s);
+    case 2: return launch_cm<2>(A, n_tiles, field, s);
+    case 4: return launch_cm<4>(A, n_tiles, field, s);
+    case 8: return launch_cm<8>(A, n_tiles, field, s);
+    case 12: return launch_cm<12>(A, n_tiles, field, s);
+    case 16: return launch_cm<16>(A, n_tiles, field, s);
+    case 18: return launch_cm<18>(A, n_tiles, field, s);
+    case 24: return launch_cm<24>(A, n_tiles, field, s);
+    case 32: return launch_cm<32>(A, n_tiles, field, s);
     default: return set_error(SQV_ERR_UNSUPPORTED, "no evaluator for %d classes", cm);
   }
 }

@@ -42,6 +42,7 @@ struct EvalArgs {
   int nx, ny, nz;
   float tau;
   int free_label;
+  int field;  // 7 (default) or 9: field_F7 / field_F (A/B diagnostics, env SQV_FIELD)
   uint8_t* labels;
   float* v_o;
   float* v_c;
