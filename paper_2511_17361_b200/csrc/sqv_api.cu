@@ -337,7 +337,13 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.v_o = out->v_o;
   A.v_c = out->v_c;
   if (prof) cudaEventRecord(g_prof.ev[3], s);
-  if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
+  {
+    // tcgen05 evaluator by default; SQV_EVAL=ffma selects the CUDA-core one (A/B runs)
+    const char* ev = std::getenv("SQV_EVAL");
+    const bool ffma = (ev && std::strcmp(ev, "ffma") == 0) || !eval_tc_supported(cm);
+    if (int rc = ffma ? eval_launch(A, cm, (int)FT, s) : eval_tc_launch(A, cm, (int)FT, s))
+      return rc;
+  }
   if (prof) {
     cudaEventRecord(g_prof.ev[4], s);
     g_prof.pending = true;

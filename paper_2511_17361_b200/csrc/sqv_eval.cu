@@ -25,6 +25,7 @@
 // argmax; dense grids and labels staged through shared memory and written
 // as coalesced row segments (x-fastest layout).
 #include "sqv_kernels.cuh"
+#include "sqv_pair.cuh"
 
 namespace sqv {
 
@@ -34,7 +35,6 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 256;            // primitives staged per chunk
 constexpr int kMaskWords = kChunk / 32;
-constexpr int kVPT = 4;                // voxels per thread (consecutive z)
 
 template <int CM>
 struct EvalShape {
@@ -113,45 +113,8 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
         const int j = q * 32 + __ffs(m) - 1;
         m &= m - 1;
         const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
-        const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
-        const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
-        // hi parts: exact; lo parts: small
-        float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
-        float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
-        float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
-        float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
-        float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
-        float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
-        const float mcut = R.mcut;
-        const int loz = R.lo[2], hiz = R.hi[2];
-        float p0[kVPT], p1[kVPT], p2[kVPT];
-        bool live[kVPT];
-        bool any = false;
-#pragma unroll
-        for (int v = 0; v < kVPT; ++v) {
-          p0[v] = h0 + l0;
-          p1[v] = h1 + l1;
-          p2[v] = h2 + l2;
-          h0 += R.H[2];
-          h1 += R.H[5];
-          h2 += R.H[8];
-          l0 += R.L[2];
-          l1 += R.L[5];
-          l2 += R.L[8];
-          const int z = z0 + v;
-          const float mm = fmaxf(fmaxf(fabsf(p0[v]), fabsf(p1[v])), fabsf(p2[v]));
-          live[v] = in_xy && z >= loz && z <= hiz && mm <= mcut;
-          any |= live[v];
-        }
-        if (!__any_sync(0xffffffffu, any)) continue;
-        const float a = R.a, b = R.b, c = R.c;
         float w[kVPT];
-#pragma unroll
-        for (int v = 0; v < kVPT; ++v) {
-          const float F = FIELD == 7 ? field_F7(p0[v], p1[v], p2[v], a, b, c)
-                                     : field_F(p0[v], p1[v], p2[v], a, b, c);
-          w[v] = (live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;
-        }
+        if (!pair_weights<FIELD>(R, x, y, z0, w)) continue;
         const float4* lw = reinterpret_cast<const float4*>(s_lw + j * S::kLRow);
 #pragma unroll
         for (int k4 = 0; k4 < S::kLRow / 4; ++k4) {

@@ -1,0 +1,356 @@
+// sqv_eval_tc.cu — K5 on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Same tile/warp/lane decomposition and the same per-pair weights as the
+// FFMA evaluator (sqv_pair.cuh), but the accumulation
+//
+//     [v_c | v_o](voxel, :) += w(voxel, prim) * [c_prim | sigma_prim]
+//
+// is what it is — a GEMM, W[128 voxels x K prims] * L[K prims x 32] per warp —
+// so it runs as tcgen05.mma.kind::tf32 with the accumulator in TMEM:
+//
+//   * each warp owns one M=128 block (its 4x4x8 voxels: row = lane*4 + v);
+//   * for every primitive its 128 weights go to the warp's A operand in shared
+//     memory and the primitive's class weights + sigma to the warp's B operand
+//     (N = 32); both K-major "interleaved" (8-row x 16-byte core matrices).
+//     Weights are buffered in registers for 4 primitives and written as one
+//     conflict-free STS.128 per row (row = voxel slot * 32 + lane);
+//   * every K = 8 primitives one elected lane issues three MMAs — W_hi*L_hi,
+//     W_hi*L_lo, W_lo*L_hi (3xTF32 split: hi = top 11 bits, lo = remainder) —
+//     and commits them to the warp's mbarrier; the A/B buffers are reused once
+//     that barrier flips;
+//   * D (128 x 32 fp32) lives in TMEM columns [32*warp, 32*warp + 32).
+//
+// The split products carry ~2^-21 relative error per term (vs 2^-24 for FFMA)
+// — two orders below the 1e-5 density tolerance — and every voxel still sums
+// its primitives in ascending order within each K step, so results are
+// deterministic.  Epilogue: tcgen05.ld (warp w reads TMEM lanes 32*(w%4)..+31)
+// -> finalize (tau, first argmax) -> staged coalesced stores.
+#include "sqv_kernels.cuh"
+#include "sqv_pair.cuh"
+#include "sqv_tc.cuh"
+
+namespace sqv {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = 8;
+constexpr int kChunk = 112;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
+constexpr int kMaskWords = (kChunk + 31) / 32;
+constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
+constexpr int kN = 32;       // class weights + sigma, padded
+constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
+constexpr uint32_t kIdesc = tc::idesc_tf32_kk(128, kN);
+
+template <int CM>
+struct TcShape {
+  static_assert(CM + 1 <= kN, "sigma column must fit in N");
+  static constexpr int kLRow = (CM + 1 + 3) & ~3;
+  // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
+  static constexpr int kA = 0;
+  static constexpr int kB = kA + kWarps * 2 * 4096;
+  static constexpr int kRec = kB + kWarps * 2 * 1024;
+  static constexpr int kLw = kRec + kChunk * kRecWords * 4;
+  static constexpr int kMask = kLw + kChunk * kLRow * 4;
+  static constexpr int kBar = (kMask + kWarps * kMaskWords * 4 + 7) & ~7;
+  static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
+  static constexpr int kEnd = kMisc + 4 + kWarps * 4;
+  static constexpr int kStage = 1024 * (CM * 4 + 4 + 1);  // epilogue staging (aliases kA..)
+  static constexpr int kBody = kEnd > kStage ? kEnd : kStage;
+  static constexpr int kSmem = kBody + 1024;               // + alignment slack
+  static_assert(kSmem <= 113 * 1024, "two CTAs per SM");
+  static_assert(kStage <= kMisc, "staging must not overwrite the flags");
+};
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+template <int CM, int FIELD>
+__global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
+  using S = TcShape<CM>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  float* s_rec = reinterpret_cast<float*>(smem + S::kRec);
+  float* s_lw = reinterpret_cast<float*>(smem + S::kLw);
+  unsigned* s_mask = reinterpret_cast<unsigned*>(smem + S::kMask);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
+  int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
+
+  const int tile_g = blockIdx.x;
+  const int f = tile_g / A.tiles_per_frame;
+  const int t = tile_g - f * A.tiles_per_frame;
+  const int tx = t % A.ntx;
+  const int ty = (t / A.ntx) % A.nty;
+  const int tz = t / (A.ntx * A.nty);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bx0 = tx * kTileX + (warp & 1) * 4;
+  const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
+  const int bz0 = tz * kTileZ + (warp >> 2) * 8;
+  const int x = bx0 + (lane & 3);
+  const int y = by0 + ((lane >> 2) & 3);
+  const int z0 = bz0 + (lane >> 4) * 4;
+
+  // ---- TMEM + barriers ----
+  if (warp == 0) {
+    tc::tmem_alloc(s_tmem, kTmemCols);
+    tc::tmem_relinquish();
+  }
+  if (lane == 0) tc::mbar_init(&s_bar[warp], 1);
+  if (tid == 0) tc::fence_mbar_init();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *s_tmem;
+  const uint32_t d_tmem = tmem_base + (uint32_t)(warp * kN);
+
+  uint8_t* a_hi = smem + S::kA + warp * 8192;
+  uint8_t* a_lo = a_hi + 4096;
+  uint8_t* b_hi = smem + S::kB + warp * 2048;
+  uint8_t* b_lo = b_hi + 1024;
+  // K-major interleaved: A 128 rows (LBO 2048, SBO 128), B 32 rows (LBO 512, SBO 128)
+  const uint64_t da_hi = tc::smem_desc_kmajor(tc::smem_u32(a_hi), 2048, 128);
+  const uint64_t da_lo = tc::smem_desc_kmajor(tc::smem_u32(a_lo), 2048, 128);
+  const uint64_t db_hi = tc::smem_desc_kmajor(tc::smem_u32(b_hi), 512, 128);
+  const uint64_t db_lo = tc::smem_desc_kmajor(tc::smem_u32(b_lo), 512, 128);
+  // 4-primitive register buffers: wb[slot][v] weights of voxel slot v, cb[slot] class weight
+  float wb[4][kVPT], cb[4];
+
+  int kk = 0;            // primitives in the open K step
+  int groups = 0;        // K steps issued by this warp
+  uint32_t phase = 0;    // parity of the next mbarrier completion to wait for
+  bool pending = false;  // an issued K step not yet known complete
+
+  auto wait_free = [&]() {
+    if (pending) {
+      tc::mbar_wait(&s_bar[warp], phase);
+      phase ^= 1u;
+      pending = false;
+    }
+  };
+
+  // write the 4 buffered primitives as K chunk c (k = 4c..4c+3) of the open step
+  auto flush = [&](int c) {
+    if (c == 0) wait_free();  // the previous step's MMAs must have read A/B
+#pragma unroll
+    for (int v = 0; v < kVPT; ++v) {
+      const uint32_t o = tc::kmajor_chunk(v * 32 + lane, c, 128);
+      float4 h, l;
+      h.x = tf32_hi(wb[0][v]);
+      h.y = tf32_hi(wb[1][v]);
+      h.z = tf32_hi(wb[2][v]);
+      h.w = tf32_hi(wb[3][v]);
+      l.x = wb[0][v] - h.x;
+      l.y = wb[1][v] - h.y;
+      l.z = wb[2][v] - h.z;
+      l.w = wb[3][v] - h.w;
+      *reinterpret_cast<float4*>(a_hi + o) = h;
+      *reinterpret_cast<float4*>(a_lo + o) = l;
+    }
+    const uint32_t ob = tc::kmajor_chunk(lane, c, 32);
+    float4 h, l;
+    h.x = tf32_hi(cb[0]);
+    h.y = tf32_hi(cb[1]);
+    h.z = tf32_hi(cb[2]);
+    h.w = tf32_hi(cb[3]);
+    l.x = cb[0] - h.x;
+    l.y = cb[1] - h.y;
+    l.z = cb[2] - h.z;
+    l.w = cb[3] - h.w;
+    *reinterpret_cast<float4*>(b_hi + ob) = h;
+    *reinterpret_cast<float4*>(b_lo + ob) = l;
+  };
+  auto issue = [&]() {
+    tc::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tc::fence_after_sync();
+      tc::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, groups > 0 ? 1u : 0u);
+      tc::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
+      tc::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, 1u);
+      tc::mma_commit(&s_bar[warp]);
+    }
+    __syncwarp();
+    ++groups;
+    pending = true;
+    kk = 0;
+  };
+  const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
+  const int64_t fbase = (int64_t)f * A.n_prims;
+  for (int c0 = beg; c0 < end; c0 += kChunk) {
+    const int n = min(kChunk, end - c0);
+    __syncthreads();
+    for (int idx = tid; idx < n * (kRecWords / 4); idx += kThreads) {
+      const int j = idx / (kRecWords / 4), q = idx - j * (kRecWords / 4);
+      const int64_t g = fbase + A.prim_ids[c0 + j];
+      reinterpret_cast<float4*>(s_rec)[idx] =
+          __ldg(reinterpret_cast<const float4*>(A.recs + g * kRecWords) + q);
+    }
+    for (int idx = tid; idx < n * (S::kLRow / 4); idx += kThreads) {
+      const int j = idx / (S::kLRow / 4), q = idx - j * (S::kLRow / 4);
+      const int64_t g = fbase + A.prim_ids[c0 + j];
+      reinterpret_cast<float4*>(s_lw)[idx] =
+          __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + q);
+    }
+    __syncthreads();
+    for (int q = 0; q * 32 < n; ++q) {
+      const int j = q * 32 + lane;
+      bool hit = false;
+      if (j < n) {
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        hit = !(bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
+                bz0 + 7 < R.lo[2] || bz0 > R.hi[2]);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_mask[warp * kMaskWords + q] = m;
+    }
+    __syncwarp();
+    for (int q = 0; q * 32 < n; ++q) {
+      unsigned m = s_mask[warp * kMaskWords + q];
+      while (m) {
+        const int j = q * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        float w[kVPT];
+        if (!pair_weights<FIELD>(R, x, y, z0, w)) continue;
+        // class weight n = lane (sigma at CM), zero beyond
+        const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
+        switch (kk & 3) {  // warp-uniform
+          case 0: wb[0][0] = w[0]; wb[0][1] = w[1]; wb[0][2] = w[2]; wb[0][3] = w[3]; cb[0] = cw; break;
+          case 1: wb[1][0] = w[0]; wb[1][1] = w[1]; wb[1][2] = w[2]; wb[1][3] = w[3]; cb[1] = cw; break;
+          case 2: wb[2][0] = w[0]; wb[2][1] = w[1]; wb[2][2] = w[2]; wb[2][3] = w[3]; cb[2] = cw; break;
+          default: wb[3][0] = w[0]; wb[3][1] = w[1]; wb[3][2] = w[2]; wb[3][3] = w[3]; cb[3] = cw; break;
+        }
+        if ((kk & 3) == 3) flush(kk >> 2);
+        if (++kk == kK) issue();
+      }
+    }
+  }
+  if (kk > 0) {  // close the last K step with zero columns
+#pragma unroll
+    for (int sl = 1; sl < 4; ++sl)
+      if (sl >= (kk & 3)) {
+        cb[sl] = 0.0f;
+#pragma unroll
+        for (int v = 0; v < kVPT; ++v) wb[sl][v] = 0.0f;
+      }
+    if ((kk & 3) != 0) flush(kk >> 2);
+    if (kk <= 4) {  // K chunk 1 entirely empty
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        cb[sl] = 0.0f;
+#pragma unroll
+        for (int v = 0; v < kVPT; ++v) wb[sl][v] = 0.0f;
+      }
+      flush(1);
+    }
+    issue();
+  }
+  wait_free();
+  if (lane == 0) s_has[warp] = groups > 0;
+  tc::fence_before_sync();
+  __syncthreads();  // all MMAs complete; operand smem is free for staging
+  tc::fence_after_sync();
+
+  // ---- epilogue: TMEM -> finalize -> staged coalesced stores -------------
+  const int C = A.n_classes;
+  const int nx = A.nx, ny = A.ny, nz = A.nz;
+  const int x_t = tx * kTileX, y_t = ty * kTileY, z_t = tz * kTileZ;
+  float* s_vc = reinterpret_cast<float*>(smem);        // [1024][C]
+  float* s_vo = s_vc + 1024 * C;                       // [1024]
+  uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 1024);
+  const int qd = warp & 3;  // TMEM lane quarter this warp may access
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int mb = (warp & 4) + i;  // M block (= producing warp)
+    float vals[32];
+    if (s_has[mb]) {
+      tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN), vals);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
+    }
+    // TMEM lane 32*qd + lane = row = v*32 + src_lane of block mb
+    const int src = lane, v = qd;
+    const int vx = (mb & 1) * 4 + (src & 3);
+    const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
+    const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
+    const int loc = vx + kTileX * (vy + kTileY * vz);
+    int best = 0;
+    float bv = vals[0];
+#pragma unroll
+    for (int k = 1; k < CM; ++k)
+      if (k < C && vals[k] > bv) {
+        bv = vals[k];
+        best = k;
+      }
+    const float vo = vals[CM];
+    if (A.v_c) {
+#pragma unroll
+      for (int k = 0; k < CM; ++k)
+        if (k < C) s_vc[loc * C + k] = vals[k];
+    }
+    s_vo[loc] = vo;
+    s_lab[loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem_base, kTmemCols);
+  }
+  const int64_t V = (int64_t)nx * ny * nz;
+  const int xw = min(kTileX, nx - x_t);
+  for (int row = warp; row < 128; row += kWarps) {  // 16 z x 8 y rows of 8 voxels
+    const int yl = row & 7, zl = row >> 3;
+    const int yy = y_t + yl, zz = z_t + zl;
+    if (yy >= ny || zz >= nz) continue;
+    const int64_t gv = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * zz);
+    if (A.v_c) {
+      const int nel = xw * C;
+      const float* src = s_vc + row * kTileX * C;
+      float* dst = A.v_c + gv * C;
+      for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+    }
+    if (lane < xw) {
+      if (A.v_o) A.v_o[gv + lane] = s_vo[row * kTileX + lane];
+      A.labels[gv + lane] = s_lab[row * kTileX + lane];
+    }
+  }
+}
+
+template <int CM>
+int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
+  using S = TcShape<CM>;
+  // never more than two CTAs per SM: each holds 256 of the 512 TMEM columns
+  constexpr int smem = S::kSmem > 80 * 1024 ? S::kSmem : 80 * 1024;
+  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : eval_tc_kernel<CM, 7>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess)
+    return check_launch("eval_tc_kernel attribute");
+  kern<<<n_tiles, kThreads, smem, s>>>(A);
+  count_launch();
+  return check_launch("eval_tc_kernel");
+}
+
+}  // namespace
+
+bool eval_tc_supported(int cm) { return cm <= 24; }
+
+int eval_tc_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
+  if (n_tiles <= 0) return SQV_OK;
+  const int field = A.field == 9 ? 9 : 7;
+  switch (cm) {
+    case 2: return launch_tc<2>(A, n_tiles, field, s);
+    case 4: return launch_tc<4>(A, n_tiles, field, s);
+    case 8: return launch_tc<8>(A, n_tiles, field, s);
+    case 12: return launch_tc<12>(A, n_tiles, field, s);
+    case 16: return launch_tc<16>(A, n_tiles, field, s);
+    case 18: return launch_tc<18>(A, n_tiles, field, s);
+    case 24: return launch_tc<24>(A, n_tiles, field, s);
+    default: return set_error(SQV_ERR_UNSUPPORTED, "no tensor-core evaluator for %d classes", cm);
+  }
+}
+
+}  // namespace sqv

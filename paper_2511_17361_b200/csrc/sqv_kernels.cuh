@@ -67,6 +67,9 @@ int radix_sort(uint32_t* keys, int* vals, uint32_t* keys_alt, int* vals_alt, int
 // evaluator
 int eval_cm_for(int C);  // padded class count for C (0 if unsupported)
 int eval_launch(const EvalArgs& A, int cm, int n_tiles_total, cudaStream_t s);
+// tensor-core (tcgen05) evaluator, CM <= 24
+bool eval_tc_supported(int cm);
+int eval_tc_launch(const EvalArgs& A, int cm, int n_tiles_total, cudaStream_t s);
 
 // misc kernels
 int finalize_launch(const float* v_o, const float* v_c, int64_t n, int C, float tau, int free_label,
