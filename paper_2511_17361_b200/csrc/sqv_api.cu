@@ -330,8 +330,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.tau = tau_f32(cfg->tau);
   A.free_label = cfg->free_label;
   {
-    const char* fe = std::getenv("SQV_FIELD");  // diagnostics only: 9 = reference 9-MUFU form
-    A.field = (fe && std::atoi(fe) == 9) ? 9 : 7;
+    const char* fe = std::getenv("SQV_FIELD");  // diagnostics only: 9 = 9-MUFU form, 8 = SFU log1p
+    A.field = fe ? std::atoi(fe) : 7;
   }
   A.labels = out->labels;
   A.v_o = out->v_o;

@@ -78,15 +78,17 @@ __device__ __forceinline__ float field_F(float x0, float x1, float x2, float a, 
 // log2(1 + t) for t in [0, 1] on the FMA pipe: degree-8 minimax (max error
 // 4.6e-8 in exact arithmetic, ~1.7e-7 evaluated in FP32, comparable to one
 // MUFU.LG2).  The leading term is applied with an FMA.
+// Estrin evaluation (dependency depth 4 instead of 7).
 __device__ __forceinline__ float log2_1p_poly(float t) {
-  float q = -9.309163317e-03f;
-  q = fmaf(q, t, 5.205900222e-02f);
-  q = fmaf(q, t, -1.375213563e-01f);
-  q = fmaf(q, t, 2.418647856e-01f);
-  q = fmaf(q, t, -3.473010957e-01f);
-  q = fmaf(q, t, 4.786837101e-01f);
-  q = fmaf(q, t, -7.211657763e-01f);
-  return fmaf(t, 1.442689896e+00f, t * (t * q));
+  const float t2 = t * t;
+  const float p01 = fmaf(4.786837101e-01f, t, -7.211657763e-01f);   // c2 t + c1
+  const float p23 = fmaf(2.418647856e-01f, t, -3.473010957e-01f);   // c4 t + c3
+  const float p45 = fmaf(5.205900222e-02f, t, -1.375213563e-01f);   // c6 t + c5
+  const float t4 = t2 * t2;
+  const float q03 = fmaf(p23, t2, p01);
+  const float q47 = fmaf(-9.309163317e-03f, t2, p45);               // c7 t^2 + p45
+  const float q = fmaf(q47, t4, q03);                                // c1 + c2 t + ... + c7 t^6
+  return fmaf(t, 1.442689896e+00f, t2 * q);
 }
 
 // The same field with 7 SFU ops instead of 8 (caller's exp excluded):
@@ -102,6 +104,20 @@ __device__ __forceinline__ float field_F7(float x0, float x1, float x2, float a,
   const float d = fmaxf(fminf(ux, uy) - umax, -126.0f);
   const float t = ex2(d);
   const float Sb = ex2(b * (umax + log2_1p_poly(t)));
+  const float Z = ex2(c * lg2(fabsf(x2)));
+  return Sb + Z;
+}
+
+// Variant with log2(1 + t) on the SFU instead of the polynomial: 8 MUFU,
+// shorter dependency chain, MUFU.LG2 absolute error (2^-22) in place of the
+// polynomial's ~1.7e-7.
+__device__ __forceinline__ float field_F8(float x0, float x1, float x2, float a, float b,
+                                          float c) {
+  const float ux = a * lg2(fabsf(x0));
+  const float uy = a * lg2(fabsf(x1));
+  const float umax = fmaxf(ux, uy);
+  const float d = fmaxf(fminf(ux, uy) - umax, -126.0f);
+  const float Sb = ex2(b * (umax + lg2(1.0f + ex2(d))));
   const float Z = ex2(c * lg2(fabsf(x2)));
   return Sb + Z;
 }

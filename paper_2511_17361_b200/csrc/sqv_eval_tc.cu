@@ -11,9 +11,9 @@
 //   * each warp owns one M=128 block (its 4x4x8 voxels: row = lane*4 + v);
 //   * for every primitive its 128 weights go to the warp's A operand in shared
 //     memory and the primitive's class weights + sigma to the warp's B operand
-//     (N = 32); both K-major "interleaved" (8-row x 16-byte core matrices).
-//     Weights are buffered in registers for 4 primitives and written as one
-//     conflict-free STS.128 per row (row = voxel slot * 32 + lane);
+//     (N = 32), both MN-major in the 128B_BASE32B swizzle (the MN-major mode
+//     tf32 supports): one conflict-free STS.128 per lane for A (row =
+//     lane*4 + voxel slot), one STS.32 per lane for B;
 //   * every K = 8 primitives one elected lane issues three MMAs — W_hi*L_hi,
 //     W_hi*L_lo, W_lo*L_hi (3xTF32 split: hi = top 11 bits, lo = remainder) —
 //     and commits them to the warp's mbarrier; the A/B buffers are reused once
@@ -40,7 +40,7 @@ constexpr int kMaskWords = (kChunk + 31) / 32;
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
 constexpr int kN = 32;       // class weights + sigma, padded
 constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
-constexpr uint32_t kIdesc = tc::idesc_tf32_kk(128, kN);
+constexpr uint32_t kIdesc = tc::idesc_tf32(128, kN, 1, 1);
 
 template <int CM>
 struct TcShape {
@@ -109,13 +109,11 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint8_t* a_lo = a_hi + 4096;
   uint8_t* b_hi = smem + S::kB + warp * 2048;
   uint8_t* b_lo = b_hi + 1024;
-  // K-major interleaved: A 128 rows (LBO 2048, SBO 128), B 32 rows (LBO 512, SBO 128)
-  const uint64_t da_hi = tc::smem_desc_kmajor(tc::smem_u32(a_hi), 2048, 128);
-  const uint64_t da_lo = tc::smem_desc_kmajor(tc::smem_u32(a_lo), 2048, 128);
-  const uint64_t db_hi = tc::smem_desc_kmajor(tc::smem_u32(b_hi), 512, 128);
-  const uint64_t db_lo = tc::smem_desc_kmajor(tc::smem_u32(b_lo), 512, 128);
-  // 4-primitive register buffers: wb[slot][v] weights of voxel slot v, cb[slot] class weight
-  float wb[4][kVPT], cb[4];
+  // MN-major BASE32B: A 128 rows (LBO 512, SBO 2048), B 32 rows (LBO 512, SBO 512)
+  const uint64_t da_hi = tc::smem_desc_mn32(tc::smem_u32(a_hi), 512, 2048);
+  const uint64_t da_lo = tc::smem_desc_mn32(tc::smem_u32(a_lo), 512, 2048);
+  const uint64_t db_hi = tc::smem_desc_mn32(tc::smem_u32(b_hi), 512, 512);
+  const uint64_t db_lo = tc::smem_desc_mn32(tc::smem_u32(b_lo), 512, 512);
 
   int kk = 0;            // primitives in the open K step
   int groups = 0;        // K steps issued by this warp
@@ -130,36 +128,24 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     }
   };
 
-  // write the 4 buffered primitives as K chunk c (k = 4c..4c+3) of the open step
-  auto flush = [&](int c) {
-    if (c == 0) wait_free();  // the previous step's MMAs must have read A/B
-#pragma unroll
-    for (int v = 0; v < kVPT; ++v) {
-      const uint32_t o = tc::kmajor_chunk(v * 32 + lane, c, 128);
-      float4 h, l;
-      h.x = tf32_hi(wb[0][v]);
-      h.y = tf32_hi(wb[1][v]);
-      h.z = tf32_hi(wb[2][v]);
-      h.w = tf32_hi(wb[3][v]);
-      l.x = wb[0][v] - h.x;
-      l.y = wb[1][v] - h.y;
-      l.z = wb[2][v] - h.z;
-      l.w = wb[3][v] - h.w;
-      *reinterpret_cast<float4*>(a_hi + o) = h;
-      *reinterpret_cast<float4*>(a_lo + o) = l;
-    }
-    const uint32_t ob = tc::kmajor_chunk(lane, c, 32);
+  // primitive in K slot k: A rows lane*4 + v (one STS.128), B row lane
+  auto store_k = [&](int k, const float(&w)[kVPT], float cw) {
+    const uint32_t ao = tc::mn32_offset(lane * 4, k, 128);
     float4 h, l;
-    h.x = tf32_hi(cb[0]);
-    h.y = tf32_hi(cb[1]);
-    h.z = tf32_hi(cb[2]);
-    h.w = tf32_hi(cb[3]);
-    l.x = cb[0] - h.x;
-    l.y = cb[1] - h.y;
-    l.z = cb[2] - h.z;
-    l.w = cb[3] - h.w;
-    *reinterpret_cast<float4*>(b_hi + ob) = h;
-    *reinterpret_cast<float4*>(b_lo + ob) = l;
+    h.x = tf32_hi(w[0]);
+    h.y = tf32_hi(w[1]);
+    h.z = tf32_hi(w[2]);
+    h.w = tf32_hi(w[3]);
+    l.x = w[0] - h.x;
+    l.y = w[1] - h.y;
+    l.z = w[2] - h.z;
+    l.w = w[3] - h.w;
+    *reinterpret_cast<float4*>(a_hi + ao) = h;
+    *reinterpret_cast<float4*>(a_lo + ao) = l;
+    const uint32_t bo = tc::mn32_offset(lane, k, 32);
+    const float ch = tf32_hi(cw);
+    *reinterpret_cast<float*>(b_hi + bo) = ch;
+    *reinterpret_cast<float*>(b_lo + bo) = cw - ch;
   };
   auto issue = [&]() {
     tc::fence_proxy_async_smem();
@@ -216,35 +202,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         if (!pair_weights<FIELD>(R, x, y, z0, w)) continue;
         // class weight n = lane (sigma at CM), zero beyond
         const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
-        switch (kk & 3) {  // warp-uniform
-          case 0: wb[0][0] = w[0]; wb[0][1] = w[1]; wb[0][2] = w[2]; wb[0][3] = w[3]; cb[0] = cw; break;
-          case 1: wb[1][0] = w[0]; wb[1][1] = w[1]; wb[1][2] = w[2]; wb[1][3] = w[3]; cb[1] = cw; break;
-          case 2: wb[2][0] = w[0]; wb[2][1] = w[1]; wb[2][2] = w[2]; wb[2][3] = w[3]; cb[2] = cw; break;
-          default: wb[3][0] = w[0]; wb[3][1] = w[1]; wb[3][2] = w[2]; wb[3][3] = w[3]; cb[3] = cw; break;
-        }
-        if ((kk & 3) == 3) flush(kk >> 2);
+        if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
+        store_k(kk, w, cw);
         if (++kk == kK) issue();
       }
     }
   }
   if (kk > 0) {  // close the last K step with zero columns
-#pragma unroll
-    for (int sl = 1; sl < 4; ++sl)
-      if (sl >= (kk & 3)) {
-        cb[sl] = 0.0f;
-#pragma unroll
-        for (int v = 0; v < kVPT; ++v) wb[sl][v] = 0.0f;
-      }
-    if ((kk & 3) != 0) flush(kk >> 2);
-    if (kk <= 4) {  // K chunk 1 entirely empty
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl) {
-        cb[sl] = 0.0f;
-#pragma unroll
-        for (int v = 0; v < kVPT; ++v) wb[sl][v] = 0.0f;
-      }
-      flush(1);
-    }
+    const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = kk; k < kK; ++k) store_k(k, zw, 0.0f);
     issue();
   }
   wait_free();
@@ -271,8 +237,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
     }
-    // TMEM lane 32*qd + lane = row = v*32 + src_lane of block mb
-    const int src = lane, v = qd;
+    // TMEM lane 32*qd + lane = row = src_lane*4 + v of block mb
+    const int src = qd * 8 + (lane >> 2), v = lane & 3;
     const int vx = (mb & 1) * 4 + (src & 3);
     const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
     const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
@@ -325,7 +291,7 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = TcShape<CM>;
   // never more than two CTAs per SM: each holds 256 of the 512 TMEM columns
   constexpr int smem = S::kSmem > 80 * 1024 ? S::kSmem : 80 * 1024;
-  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : eval_tc_kernel<CM, 7>;
+  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : field == 8 ? eval_tc_kernel<CM, 8> : eval_tc_kernel<CM, 7>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess)
     return check_launch("eval_tc_kernel attribute");
@@ -340,7 +306,7 @@ bool eval_tc_supported(int cm) { return cm <= 24; }
 
 int eval_tc_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return SQV_OK;
-  const int field = A.field == 9 ? 9 : 7;
+  const int field = (A.field == 9 || A.field == 8) ? A.field : 7;
   switch (cm) {
     case 2: return launch_tc<2>(A, n_tiles, field, s);
     case 4: return launch_tc<4>(A, n_tiles, field, s);

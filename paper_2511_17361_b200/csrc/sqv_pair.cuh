@@ -22,12 +22,13 @@ __device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int
                                              float (&w)[kVPT]) {
   const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
-  float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
-  float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
-  float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
-  float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
-  float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
-  float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
+  // column base (z0) then each voxel directly: hi parts exact, short chains
+  const float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
+  const float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
+  const float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
+  const float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
+  const float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
+  const float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
   const float mcut = R.mcut;
   const int loz = R.lo[2], hiz = R.hi[2];
   float p0[kVPT], p1[kVPT], p2[kVPT];
@@ -35,15 +36,10 @@ __device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int
   bool any = false;
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
-    p0[v] = h0 + l0;
-    p1[v] = h1 + l1;
-    p2[v] = h2 + l2;
-    h0 += R.H[2];
-    h1 += R.H[5];
-    h2 += R.H[8];
-    l0 += R.L[2];
-    l1 += R.L[5];
-    l2 += R.L[8];
+    const float fv = (float)v;
+    p0[v] = fmaf(fv, R.H[2], h0) + fmaf(fv, R.L[2], l0);
+    p1[v] = fmaf(fv, R.H[5], h1) + fmaf(fv, R.L[5], l1);
+    p2[v] = fmaf(fv, R.H[8], h2) + fmaf(fv, R.L[8], l2);
     const int z = z0 + v;
     const float mm = fmaxf(fmaxf(fabsf(p0[v]), fabsf(p1[v])), fabsf(p2[v]));
     live[v] = in_xy && z >= loz && z <= hiz && mm <= mcut;
@@ -53,8 +49,9 @@ __device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int
   const float a = R.a, b = R.b, c = R.c;
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
-    const float F = FIELD == 7 ? field_F7(p0[v], p1[v], p2[v], a, b, c)
-                               : field_F(p0[v], p1[v], p2[v], a, b, c);
+    const float F = FIELD == 7   ? field_F7(p0[v], p1[v], p2[v], a, b, c)
+                    : FIELD == 8 ? field_F8(p0[v], p1[v], p2[v], a, b, c)
+                                 : field_F(p0[v], p1[v], p2[v], a, b, c);
     w[v] = (live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;
   }
   return true;

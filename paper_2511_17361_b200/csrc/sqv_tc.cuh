@@ -91,14 +91,33 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M x N.  (MN-major
-// tf32 operands read as zeros on sm_100a in tests/cuda/umma_probe.cu, so
-// every operand here is K-major.)
-__host__ __device__ constexpr uint32_t idesc_tf32_kk(int M, int N) {
+// Instruction descriptor: D f32, A/B tf32, M x N; a_mn/b_mn select
+// MN-major operands (bits 15/16).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
   return (1u << 4)                  // D format f32
          | (2u << 7)                // A format tf32
          | (2u << 10)               // B format tf32
-         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+         | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// MN-major 32-bit operands need the SWIZZLE_128B_BASE32B mode (layout type
+// 1; every other MN-major encoding reads zeros for tf32 — pinned by
+// tests/cuda/umma_probe.cu).  Canonical form: 128-byte rows of 32 mn
+// elements, 4 k-rows per 512-byte atom, the four 32-byte chunks of a row
+// XOR-ed with the row index; LBO = stride between mn atoms, SBO = stride
+// between groups of 4 k.
+__device__ __forceinline__ uint64_t smem_desc_mn32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (1ull << 61);
+}
+
+// Byte offset of element (mn, k) in such an operand with `mn_extent` rows
+// (mn atoms 512 B apart, k groups mn_extent*16 B apart).  Elements mn..mn+3
+// (mn % 4 == 0) are 16 contiguous bytes.
+__device__ __forceinline__ uint32_t mn32_offset(int mn, int k, int mn_extent) {
+  return (uint32_t)((k >> 2) * mn_extent * 16 + (mn >> 5) * 512 + (k & 3) * 128 +
+                    ((((mn >> 3) & 3) ^ (k & 3)) << 5) + ((mn & 7) << 2));
 }
 
 // Shared-memory matrix descriptor, SWIZZLE_NONE ("interleaved"), sm_100

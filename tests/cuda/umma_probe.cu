@@ -18,6 +18,8 @@ using namespace sqv;
 //  1: MN-major, SWIZZLE_128B (rows of 128 B = 32 mn; 8 k-rows per 1 KB atom; LBO = 1024)
 //  2: MN-major, SWIZZLE_NONE (core matrix 4 mn x 8 k = 128 B; SBO = 128 along mn)
 //  3: K-major, SWIZZLE_NONE  (core matrix 8 mn x 4 k = 128 B; LBO = k-chunk stride, SBO = 128)
+//  4: MN-major, SWIZZLE_128B_BASE32B (rows of 128 B = 32 mn, 4 k-rows per 512 B atom,
+//     32-byte chunks XOR row; LBO = mn-atom stride 512, SBO = k-group stride)
 struct Lay {
   int id;
   uint32_t lbo, sbo;
@@ -30,7 +32,10 @@ __device__ uint32_t off_of(int id, int mn, int k, int mn_extent) {
     case 0: return (uint32_t)((mn >> 3) * 256 + (mn & 7) * 32 + ((((k >> 2) ^ ((mn >> 2) & 1))) << 4) + ((k & 3) << 2));
     case 1: return (uint32_t)((mn >> 5) * 1024 + k * 128 + ((((mn >> 2) & 7) ^ k) << 4) + ((mn & 3) << 2));
     case 2: return (uint32_t)((mn >> 2) * 128 + k * 16 + ((mn & 3) << 2));
-    default: return tc::kmajor_chunk(mn, k >> 2, mn_extent) + ((k & 3) << 2);
+    case 3: return tc::kmajor_chunk(mn, k >> 2, mn_extent) + ((k & 3) << 2);
+    default:
+      return (uint32_t)((k >> 2) * (mn_extent / 32) * 512 + (mn >> 5) * 512 + (k & 3) * 128 +
+                        ((((mn >> 3) & 3) ^ (k & 3)) << 5) + ((mn & 7) << 2));
   }
 }
 
@@ -108,10 +113,10 @@ int main() {
   cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 24576);
   // A candidates (mn extent 128) and B candidates (mn extent 32)
-  // K-major layouts only: MN-major tf32 operands read as zeros on sm_100a
-  // (probed: every MN-major SWIZZLE_NONE / SWIZZLE_128B encoding gave D = 0).
-  const Lay As[] = {{0, 16, 256, 6, 0}, {3, 2048, 128, 0, 0}};
-  const Lay Bs[] = {{0, 16, 256, 6, 0}, {3, 512, 128, 0, 0}};
+  // MN-major tf32 works only with SWIZZLE_128B_BASE32B (layout 4); the
+  // MN-major SWIZZLE_NONE / SWIZZLE_128B encodings read zeros (probed).
+  const Lay As[] = {{0, 16, 256, 6, 0}, {3, 2048, 128, 0, 0}, {4, 512, 2048, 1, 1}};
+  const Lay Bs[] = {{0, 16, 256, 6, 0}, {3, 512, 128, 0, 0}, {4, 512, 512, 1, 1}};
   int failures = 0;
   for (const Lay& la : As)
     for (const Lay& lb : Bs) {

@@ -19,4 +19,4 @@ def test_umma_probe_layouts():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("<== OK") == 4
+    assert r.stdout.count("<== OK") == 9
