@@ -32,7 +32,8 @@ class Grid(ctypes.Structure):
 
 class Cfg(ctypes.Structure):
     _fields_ = [("tau", _f64), ("neighborhood_radius", _i32), ("truncate", _i32),
-                ("semantic_mode", _i32), ("free_label", _i32), ("window_extent", _f64)]
+                ("semantic_mode", _i32), ("free_label", _i32), ("window_extent", _f64),
+                ("precision", _i32)]
 
 
 class Prims(ctypes.Structure):

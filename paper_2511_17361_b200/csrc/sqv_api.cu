@@ -186,6 +186,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     return set_error(SQV_ERR_ARG, "window_extent must be finite and >= 0");
   if (cfg->free_label < 0 || cfg->free_label > 255 || cfg->free_label < C)
     return set_error(SQV_ERR_ARG, "free_label must lie in [C, 255]");
+  if (cfg->precision != 0 && cfg->precision != 1)
+    return set_error(SQV_ERR_ARG, "precision must be 0 (fast) or 1 (strict)");
   if (cfg->semantic_mode != 0 && cfg->semantic_mode != 1)
     return set_error(SQV_ERR_ARG, "semantic_mode must be 0 (logit-sum) or 1 (prob-sum)");
   if (F == 0) return SQV_OK;
@@ -331,7 +333,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.free_label = cfg->free_label;
   {
     const char* fe = std::getenv("SQV_FIELD");  // diagnostics only: 9 = 9-MUFU form, 8 = SFU log1p
-    A.field = fe ? std::atoi(fe) : 7;
+    A.field = fe ? std::atoi(fe) : (cfg->precision ? 6 : 7);
   }
   A.labels = out->labels;
   A.v_o = out->v_o;

@@ -122,6 +122,51 @@ __device__ __forceinline__ float field_F8(float x0, float x1, float x2, float a,
   return Sb + Z;
 }
 
+// log2(x) on the FMA pipe to ~1 ulp (vs MUFU.LG2's 2^-22 absolute error):
+// x = m 2^e with m in [sqrt(1/2), sqrt(2)), log2(m) = r q(r), r = m - 1,
+// degree-8 minimax q (relative error 2.6e-8).  Zero and denormals give -inf
+// like lg2.approx.ftz.
+__device__ __forceinline__ float log2_acc(float x) {
+  const int i = __float_as_int(x);
+  const int e = (i - 0x3f3504f3) >> 23;
+  const float r = __int_as_float(i - (e << 23)) - 1.0f;
+  float q = 1.258370578e-01f;
+  q = fmaf(q, r, -2.072697580e-01f);
+  q = fmaf(q, r, 2.157156020e-01f);
+  q = fmaf(q, r, -2.389448136e-01f);
+  q = fmaf(q, r, 2.879162431e-01f);
+  q = fmaf(q, r, -3.607036769e-01f);
+  q = fmaf(q, r, 4.809106290e-01f);
+  q = fmaf(q, r, -7.213473320e-01f);
+  q = fmaf(q, r, 1.442695022e+00f);
+  const float l = fmaf(r, q, (float)e);
+  return x >= 1.17549435e-38f ? l : -INFINITY;
+}
+
+// "strict" field: the coordinate logs go through log2_acc when the primitive
+// amplifies their error, i.e. when 2/eps1 (= c = a*b) > 3 — a warp-uniform
+// choice per primitive.  Below that the SFU logs already keep |dF| <= 5e-7 F.
+__device__ __forceinline__ float field_F6(float x0, float x1, float x2, float a, float b,
+                                          float c) {
+  float lx, ly, lz;
+  if (c > 3.0f) {
+    lx = log2_acc(fabsf(x0));
+    ly = log2_acc(fabsf(x1));
+    lz = log2_acc(fabsf(x2));
+  } else {
+    lx = lg2(fabsf(x0));
+    ly = lg2(fabsf(x1));
+    lz = lg2(fabsf(x2));
+  }
+  const float ux = a * lx, uy = a * ly;
+  const float umax = fmaxf(ux, uy);
+  const float d = fmaxf(fminf(ux, uy) - umax, -126.0f);
+  const float t = ex2(d);
+  const float Sb = ex2(b * (umax + log2_1p_poly(t)));
+  const float Z = ex2(c * lz);
+  return Sb + Z;
+}
+
 __device__ __forceinline__ float density_of(float F) {
   return F < kFCut ? ex2(-F * kLog2e) : 0.0f;
 }

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
 template <int CM>
 int launch_cm(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = EvalShape<CM>;
-  auto kern = field == 9 ? eval_kernel<CM, 9> : field == 8 ? eval_kernel<CM, 8> : eval_kernel<CM, 7>;
+  auto kern = field == 9 ? eval_kernel<CM, 9> : field == 8 ? eval_kernel<CM, 8> : field == 6 ? eval_kernel<CM, 6> : eval_kernel<CM, 7>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem) !=
       cudaSuccess)
     return check_launch("eval_kernel attribute");
@@ -225,7 +225,7 @@ int eval_cm_for(int C) {
 
 int eval_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return SQV_OK;
-  const int field = (A.field == 9 || A.field == 8) ? A.field : 7;
+  const int field = (A.field == 9 || A.field == 8 || A.field == 6) ? A.field : 7;
   switch (cm) {
     case 2: return launch_cm<2>(A, n_tiles, field, s);
     case 4: return launch_cm<4>(A, n_tiles, field, s);

@@ -291,7 +291,7 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = TcShape<CM>;
   // never more than two CTAs per SM: each holds 256 of the 512 TMEM columns
   constexpr int smem = S::kSmem > 80 * 1024 ? S::kSmem : 80 * 1024;
-  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : field == 8 ? eval_tc_kernel<CM, 8> : eval_tc_kernel<CM, 7>;
+  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : field == 8 ? eval_tc_kernel<CM, 8> : field == 6 ? eval_tc_kernel<CM, 6> : eval_tc_kernel<CM, 7>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess)
     return check_launch("eval_tc_kernel attribute");
@@ -306,7 +306,7 @@ bool eval_tc_supported(int cm) { return cm <= 24; }
 
 int eval_tc_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return SQV_OK;
-  const int field = (A.field == 9 || A.field == 8) ? A.field : 7;
+  const int field = (A.field == 9 || A.field == 8 || A.field == 6) ? A.field : 7;
   switch (cm) {
     case 2: return launch_tc<2>(A, n_tiles, field, s);
     case 4: return launch_tc<4>(A, n_tiles, field, s);

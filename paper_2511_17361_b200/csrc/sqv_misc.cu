@@ -92,7 +92,7 @@ __global__ void density_kernel(sqv_prims P, const double* __restrict__ points,
   const float x0 = (float)(Q.M[0] * d0 + Q.M[1] * d1 + Q.M[2] * d2);
   const float x1 = (float)(Q.M[3] * d0 + Q.M[4] * d1 + Q.M[5] * d2);
   const float x2 = (float)(Q.M[6] * d0 + Q.M[7] * d1 + Q.M[8] * d2);
-  const float F = field_F7(x0, x1, x2, (float)(2.0 / Q.e2), (float)(Q.e2 / Q.e1),
+  const float F = field_F6(x0, x1, x2, (float)(2.0 / Q.e2), (float)(Q.e2 / Q.e1),
                           (float)(2.0 / Q.e1));
   Fout[k] = fminf(F, kFCap);
   dout[k] = density_of(F);

@@ -50,6 +50,7 @@ __device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
     const float F = FIELD == 7   ? field_F7(p0[v], p1[v], p2[v], a, b, c)
+                    : FIELD == 6 ? field_F6(p0[v], p1[v], p2[v], a, b, c)
                     : FIELD == 8 ? field_F8(p0[v], p1[v], p2[v], a, b, c)
                                  : field_F(p0[v], p1[v], p2[v], a, b, c);
     w[v] = (live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;

@@ -114,6 +114,17 @@ def test_config1_occ3d_256():
     print("config1 worst v_o rel", vo["worst_rel"], "label agreement", lab["agreement"])
 
 
+def test_fast_precision_mode_two_tier():
+    """precision="fast" (all logs on the SFU): labels unchanged, densities within
+    the two-tier criterion."""
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig(precision="fast")
+    b = _scene(11, 256)
+    out = _run(b, spec, cfg, 18)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"])
+    assert_parity(out, ref, cfg.tau, out["free_code"], mode="fast")
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_acceptance4_bruteforce_equivalence(seed):
     """SPEC.md:630 #4: <=50 prims, 32^3: untruncated voxelize == bruteforce oracle."""
