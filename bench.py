@@ -273,7 +273,8 @@ def run_ours(a, rank, world, local_rank):
     achieved = pairs_per_launch * MUFU_PER_PAIR / eval_s
     roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                 "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": None,
-                "kernel": f"eval_kernel<{vox.C if vox.C in (2, 4, 8, 12, 16, 18, 24, 32) else 'cm'}>",
+                "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc.cu)" if os.environ.get(
+                    "SQV_EVAL") != "ffma" else "eval_kernel (FFMA, sqv_eval.cu)",
                 "algorithmic": f"{MUFU_PER_PAIR} MUFU per in-window (primitive, voxel) pair x "
                                f"{pairs_per_launch:.4e} pairs per launch",
                 "eval_ms_per_launch": eval_s * 1e3,

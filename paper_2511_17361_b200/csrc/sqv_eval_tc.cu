@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = 8;
-constexpr int kChunk = 112;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
+constexpr int kChunk = 104;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
 constexpr int kMaskWords = (kChunk + 31) / 32;
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
 constexpr int kN = 32;       // class weights + sigma, padded

@@ -23,12 +23,12 @@ __device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int
   const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
   // column base (z0) then each voxel directly: hi parts exact, short chains
-  const float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fx * R.H[0]));
-  const float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fx * R.H[3]));
-  const float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fx * R.H[6]));
-  const float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.G[0])));
-  const float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.G[1])));
-  const float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.G[2])));
+  const float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fmaf(fx, R.H[0], R.Gh[0])));
+  const float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fmaf(fx, R.H[3], R.Gh[1])));
+  const float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fmaf(fx, R.H[6], R.Gh[2])));
+  const float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.Gl[0])));
+  const float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.Gl[1])));
+  const float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.Gl[2])));
   const float mcut = R.mcut;
   const int loz = R.lo[2], hiz = R.hi[2];
   float p0[kVPT], p1[kVPT], p2[kVPT];

@@ -18,11 +18,16 @@ namespace sqv {
 // row quantum q (10 significant bits of the row's largest entry).  Then
 // k * hi is exact for |k| < 2^12 and the sum of the three hi products of a
 // row is exact in FP32, so lattice offsets never cancel catastrophically.
-__device__ inline void split_row(const double v[3], float hi[3], float lo[3]) {
+// The reference-voxel offset g of the row is split on the same quantum, so
+// g_hi + sum_j k_j * hi_j is an exact FP32 sum too.
+__device__ inline void split_row(const double v[3], double g, float hi[3], float lo[3],
+                                 float* g_hi, float* g_lo) {
   const double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fabs(v[2]));
   if (m == 0.0) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) hi[j] = lo[j] = 0.0f;
+    *g_hi = 0.0f;
+    *g_lo = (float)g;
     return;
   }
   int e;
@@ -35,6 +40,9 @@ __device__ inline void split_row(const double v[3], float hi[3], float lo[3]) {
     hi[j] = (float)h;                 // exact: <= 11 significant bits
     lo[j] = (float)(v[j] - h);
   }
+  const double gh = rint(g * iq) * q;
+  *g_hi = (float)gh;                  // exact while |g| < 2^(e+13)
+  *g_lo = (float)(g - gh);
 }
 
 __global__ void prep_kernel(PrepArgs A) {
@@ -107,8 +115,8 @@ __global__ void prep_kernel(PrepArgs A) {
 #pragma unroll
         for (int r2 = 0; r2 < 3; ++r2) {
           const double row[3] = {P.M[3 * r2] * res, P.M[3 * r2 + 1] * res, P.M[3 * r2 + 2] * res};
-          split_row(row, &rec.H[3 * r2], &rec.L[3 * r2]);
-          rec.G[r2] = (float)(P.M[3 * r2] * d[0] + P.M[3 * r2 + 1] * d[1] + P.M[3 * r2 + 2] * d[2]);
+          const double g = P.M[3 * r2] * d[0] + P.M[3 * r2 + 1] * d[1] + P.M[3 * r2 + 2] * d[2];
+          split_row(row, g, &rec.H[3 * r2], &rec.L[3 * r2], &rec.Gh[r2], &rec.Gl[r2]);
         }
         rec.a = (float)(2.0 / P.e2);
         rec.b = (float)(P.e2 / P.e1);
@@ -118,7 +126,6 @@ __global__ void prep_kernel(PrepArgs A) {
         rec.cx = (float)cref[0];
         rec.cy = (float)cref[1];
         rec.cz = (float)cref[2];
-        rec.sigma = (float)P.sigma;
         // class weights: logits (logit-sum) or softmax (prob-sum)
         if (A.cfg.semantic_mode == 1) {
           double m = logits[0];
