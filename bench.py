@@ -271,8 +271,19 @@ def run_ours(a, rank, world, local_rank):
     eval_s = prof["eval_ms"] * 1e-3 / max(prof["calls"], 1)
     pairs_per_launch = pairs / max(K, 1)
     achieved = pairs_per_launch * MUFU_PER_PAIR / eval_s
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes of the evaluator from the committed ncu --set full capture, per launch
+        import glob
+        prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_eval_tc_ncu.json")))[-1]
+        pj = json.load(open(prof))
+        traffic = (pj["dram_bytes_read"] + pj["dram_bytes_write"]) * B / pj["frames_per_launch"]
+        traffic_src = os.path.relpath(prof, ROOT) + f" (ncu {pj['frames_per_launch']}-frame launch, scaled to {B})"
+    except Exception:
+        pass
     roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
-                "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": None,
+                "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": B * spec.n_voxels * (1 + 4 + 4 * C),
                 "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc.cu)" if os.environ.get(
                     "SQV_EVAL") != "ffma" else "eval_kernel (FFMA, sqv_eval.cu)",
                 "algorithmic": f"{MUFU_PER_PAIR} MUFU per in-window (primitive, voxel) pair x "

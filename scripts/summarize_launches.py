@@ -1,0 +1,32 @@
+"""Summarise an ncu launch list (gpu__time_duration.sum per launch) by kernel."""
+import collections
+import csv
+import re
+import sys
+
+
+def short(name):
+    name = name.replace("void ", "").replace("(anonymous namespace)::", "")
+    name = re.sub(r"\(.*\)$", "", name)
+    return name.replace("sqv::", "")
+
+
+def main(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr, data = rows[0], rows[1:]
+    iK, iV, iM = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in data:
+        if r[iM] != "gpu__time_duration.sum":
+            continue
+        k = short(r[iK])
+        tot[k] += float(r[iV].replace(",", ""))
+        cnt[k] += 1
+    T = sum(tot.values())
+    print(f"{'kernel':46s} {'launches':>8s} {'total us':>11s} {'share':>7s}")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        print(f"{k:46s} {cnt[k]:8d} {v / 1e3:11.1f} {100 * v / T:6.1f}%")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
