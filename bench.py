@@ -274,10 +274,11 @@ def run_ours(a, rank, world, local_rank):
     traffic, traffic_src = None, None
     try:  # DRAM bytes of the evaluator from the committed ncu --set full capture, per launch
         import glob
-        prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_eval_tc_ncu.json")))[-1]
-        pj = json.load(open(prof))
+        ppath = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_eval_tc_ncu.json")))[-1]
+        pj = json.load(open(ppath))
         traffic = (pj["dram_bytes_read"] + pj["dram_bytes_write"]) * B / pj["frames_per_launch"]
-        traffic_src = os.path.relpath(prof, ROOT) + f" (ncu {pj['frames_per_launch']}-frame launch, scaled to {B})"
+        traffic_src = (os.path.relpath(ppath, ROOT) +
+                       f" (ncu {pj['frames_per_launch']}-frame launch, scaled to {B})")
     except Exception:
         pass
     roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,

@@ -98,9 +98,8 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
       const int j = q * 32 + lane;
       bool hit = false;
       if (j < n) {
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
-        hit = !(bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
-                bz0 + 7 < R.lo[2] || bz0 > R.hi[2]);
+        hit = block_may_hit(*reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords), bx0, by0,
+                            bz0);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (lane == 0) s_mask[warp * kMaskWords + q] = m;
