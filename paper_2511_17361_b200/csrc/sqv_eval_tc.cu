@@ -35,8 +35,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = 8;
-constexpr int kChunk = 104;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
-constexpr int kMaskWords = (kChunk + 31) / 32;
+constexpr int kMaxChunk = 128;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
+constexpr int kMaskWords = kMaxChunk / 32;
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
 constexpr int kN = 32;       // class weights + sigma, padded
 constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
@@ -46,6 +46,7 @@ template <int CM>
 struct TcShape {
   static_assert(CM + 1 <= kN, "sigma column must fit in N");
   static constexpr int kLRow = (CM + 1 + 3) & ~3;
+  static constexpr int kChunk = CM <= 18 ? 128 : 104;
   // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
   static constexpr int kA = 0;
   static constexpr int kB = kA + kWarps * 2 * 4096;
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   };
   const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
   const int64_t fbase = (int64_t)f * A.n_prims;
-  for (int c0 = beg; c0 < end; c0 += kChunk) {
-    const int n = min(kChunk, end - c0);
+  for (int c0 = beg; c0 < end; c0 += S::kChunk) {
+    const int n = min(S::kChunk, end - c0);
     __syncthreads();
     for (int idx = tid; idx < n * (kRecWords / 4); idx += kThreads) {
       const int j = idx / (kRecWords / 4), q = idx - j * (kRecWords / 4);
