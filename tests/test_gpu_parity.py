@@ -305,3 +305,21 @@ def test_confusion_large_and_iou_examples():
     assert M.voxel_iou(pred, pred) == 1.0
     per, m = M.miou(pred, pred)
     assert m == 1.0
+
+
+def test_stream_api_matches_direct_calls():
+    """Voxelizer.stream (overlapped copies) gives the same labels as direct calls."""
+    import torch
+    P = _pkg()
+    spec = P.VoxelGridSpec((-8.0, -8.0, -2.0), (40, 40, 16), 0.4)
+    vox = P.Voxelizer(spec, P.VoxelizeConfig(), 6)
+    batches = [_scene(60 + k, 150, C=6, frames=3, origin=spec.origin, dims=spec.dims, smax=2.0)
+               for k in range(4)]
+    pinned = [P.PrimitiveBatch(**{f: torch.from_numpy(np.asarray(getattr(b, f))).pin_memory()
+                                  for f in P.PrimitiveBatch.FIELDS}) for b in batches]
+    seen = []
+    labels = vox.stream(pinned, on_device=lambda k, r: seen.append(k))
+    assert seen == [0, 1, 2, 3]
+    for b, lab in zip(batches, labels):
+        direct = vox(b).labels.cpu()
+        assert torch.equal(direct, lab)
