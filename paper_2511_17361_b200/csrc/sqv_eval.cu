@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
         m &= m - 1;
         const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
         float w[kVPT];
-        if (!pair_weights<FIELD>(R, x, y, z0, w)) continue;
+        pair_weights<FIELD>(R, x, y, z0, w);
         const float4* lw = reinterpret_cast<const float4*>(s_lw + j * S::kLRow);
 #pragma unroll
         for (int k4 = 0; k4 < S::kLRow / 4; ++k4) {

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         m &= m - 1;
         const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
         float w[kVPT];
-        if (!pair_weights<FIELD>(R, x, y, z0, w)) continue;
+        pair_weights<FIELD>(R, x, y, z0, w);
         // class weight n = lane (sigma at CM), zero beyond
         const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
         if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B

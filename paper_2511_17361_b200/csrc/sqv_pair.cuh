@@ -40,18 +40,18 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
 }
 
 // Coordinates + liveness of primitive R at voxels (x, y, z0 + v), v < 4.
-// Returns false — warp-uniformly — when no lane of the warp has a live voxel:
-// outside the window, or the whole 4-voxel column lies where
-// max|x'| > mcut, so that F > kFCut and w would be exactly 0.  The column
-// test is conservative (centre minus half extent, with a relative margin far
-// above FP32 error), so it never drops a voxel the evaluation would keep.
+// The caller has already established — per warp, with block_may_hit — that
+// the primitive can reach the warp's block, so there is no further cull
+// here: a voxel is live when it is inside the window; voxels with
+// F >= kFCut get w = 0 from the field itself (exactly what culling would
+// have produced).
 //
 // Local coordinates use the exact lattice stepping of prep's split_row: the
 // hi parts (10 significant bits per row, the reference offset on the same
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
 // primitives far from their centre voxel.
-__device__ __forceinline__ bool pair_coords(const PrimRec& R, int x, int y, int z0,
+__device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords& cd) {
   const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
@@ -61,29 +61,22 @@ __device__ __forceinline__ bool pair_coords(const PrimRec& R, int x, int y, int 
   const float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.Gl[0])));
   const float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.Gl[1])));
   const float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.Gl[2])));
-  // column cull: centre (v = 1.5) and half extent 1.5 |dz| per local axis
-  const float e0 = R.H[2] + R.L[2], e1 = R.H[5] + R.L[5], e2 = R.H[8] + R.L[8];
-  const float c0 = fmaf(1.5f, e0, h0 + l0), c1 = fmaf(1.5f, e1, h1 + l1),
-              c2 = fmaf(1.5f, e2, h2 + l2);
-  const float d0 = fmaf(-1.5f, fabsf(e0), fabsf(c0)), d1 = fmaf(-1.5f, fabsf(e1), fabsf(c1)),
-              d2 = fmaf(-1.5f, fabsf(e2), fabsf(c2));
-  const float dmax = fmaxf(fmaxf(d0, d1), d2);
-  const float slack = 1e-4f * (fabsf(c0) + fabsf(c1) + fabsf(c2) + fabsf(e0) + fabsf(e1) +
-                               fabsf(e2));
   const int loz = R.lo[2], hiz = R.hi[2];
-  const bool zin = z0 + 3 >= loz && z0 <= hiz;
-  const bool alive = in_xy && zin && dmax <= R.mcut + slack;
-  if (!__any_sync(0xffffffffu, alive)) return false;
+  cd.p0[0] = h0 + l0;
+  cd.p1[0] = h1 + l1;
+  cd.p2[0] = h2 + l2;
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) {
+  for (int v = 1; v < kVPT; ++v) {
     const float fv = (float)v;
     cd.p0[v] = fmaf(fv, R.H[2], h0) + fmaf(fv, R.L[2], l0);
     cd.p1[v] = fmaf(fv, R.H[5], h1) + fmaf(fv, R.L[5], l1);
     cd.p2[v] = fmaf(fv, R.H[8], h2) + fmaf(fv, R.L[8], l2);
-    const int z = z0 + v;
-    cd.live[v] = alive && z >= loz && z <= hiz;
   }
-  return true;
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) {
+    const int z = z0 + v;
+    cd.live[v] = in_xy && z >= loz && z <= hiz;
+  }
 }
 
 // Field of one voxel with either SFU logs (ACC = false) or FMA-pipe ~1 ulp
@@ -139,12 +132,11 @@ __device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords& cd
 
 // Single-primitive convenience (coords + field).
 template <int FIELD>
-__device__ __forceinline__ bool pair_weights(const PrimRec& R, int x, int y, int z0,
+__device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int z0,
                                              float (&w)[kVPT]) {
   ColCoords cd;
-  if (!pair_coords(R, x, y, z0, cd)) return false;
+  pair_coords(R, x, y, z0, cd);
   pair_field<FIELD>(R, cd, w);
-  return true;
 }
 
 }  // namespace sqv
