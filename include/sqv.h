@@ -89,8 +89,8 @@ typedef struct sqv_cfg {
   double window_extent;        /* max K of the scaled family, default 2.5 */
   int32_t precision;           /* 1: strict (default) — coordinate logs on the FMA pipe for
                                   primitives with 2/eps1 > 3, densities within 1e-5 relative
-                                  down to 1e-3*tau; 0: fast — all logs on the SFU (~11% faster,
-                                  1e-5 relative for v_o >= tau/10, 2e-5 below) */
+                                  down to 1e-3*tau; 0: fast — all logs on the SFU (~13% faster,
+                                  2e-5 relative down to 1e-3*tau) */
 } sqv_cfg;
 
 /* Primitive batch (device pointers, FP64). */

@@ -33,6 +33,7 @@ constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
 //   mcut:             Chebyshev cull bound, F >= max|x'|^(2/eps1)
 //   cx, cy, cz:       reference voxel index (exact small integers)
 //   lo[3], hi[3]:     clipped voxel window (int)
+//   Ez[3]:            res * M'[r][2] rounded once (the fast-mode z step)
 // (sigma travels with the class weights, see prep's lrows.)
 constexpr int kRecWords = 40;
 struct __align__(16) PrimRec {
@@ -45,7 +46,7 @@ struct __align__(16) PrimRec {
   float cx, cy, cz;
   int lo[3];
   int hi[3];
-  float pad[3];
+  float Ez[3];
 };
 static_assert(sizeof(PrimRec) == kRecWords * 4, "PrimRec layout");
 

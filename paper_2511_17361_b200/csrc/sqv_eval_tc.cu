@@ -130,8 +130,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   };
 
   // primitive in K slot k: A rows lane*4 + v (one STS.128), B row lane
+  // per-lane parts of the operand offsets (tc::mn32_offset with mn = lane*4
+  // for A, mn = lane for B); the K slot adds a uniform part and a swizzle XOR
+  const uint32_t a_base = (uint32_t)((lane >> 3) * 512 + (lane & 1) * 16);
+  const uint32_t a_t = (uint32_t)(((lane >> 1) & 3) << 5);
+  const uint32_t b_base = (uint32_t)((lane & 7) * 4);
+  const uint32_t b_t = (uint32_t)(((lane >> 3) & 3) << 5);
   auto store_k = [&](int k, const float(&w)[kVPT], float cw) {
-    const uint32_t ao = tc::mn32_offset(lane * 4, k, 128);
+    const uint32_t kq = (uint32_t)(k & 3), kh = (uint32_t)(k >> 2), kx = kq << 5;
+    const uint32_t ao = a_base + kh * 2048u + kq * 128u + (a_t ^ kx);
     float4 h, l;
     h.x = tf32_hi(w[0]);
     h.y = tf32_hi(w[1]);
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     l.w = w[3] - h.w;
     *reinterpret_cast<float4*>(a_hi + ao) = h;
     *reinterpret_cast<float4*>(a_lo + ao) = l;
-    const uint32_t bo = tc::mn32_offset(lane, k, 32);
+    const uint32_t bo = b_base + kh * 512u + kq * 128u + (b_t ^ kx);
     const float ch = tf32_hi(cw);
     *reinterpret_cast<float*>(b_hi + bo) = ch;
     *reinterpret_cast<float*>(b_lo + bo) = cw - ch;
@@ -266,22 +273,27 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tmem_base, kTmemCols);
   }
+  // rows of 8 voxels: this warp owns y row y_t + warp (8 warps = the tile's
+  // 8 y rows) for every z layer, so the row base just steps by nx*ny
   const int64_t V = (int64_t)nx * ny * nz;
   const int xw = min(kTileX, nx - x_t);
-  for (int row = warp; row < 128; row += kWarps) {  // 16 z x 8 y rows of 8 voxels
-    const int yl = row & 7, zl = row >> 3;
-    const int yy = y_t + yl, zz = z_t + zl;
-    if (yy >= ny || zz >= nz) continue;
-    const int64_t gv = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * zz);
-    if (A.v_c) {
-      const int nel = xw * C;
-      const float* src = s_vc + row * kTileX * C;
-      float* dst = A.v_c + gv * C;
-      for (int e = lane; e < nel; e += 32) dst[e] = src[e];
-    }
-    if (lane < xw) {
-      if (A.v_o) A.v_o[gv + lane] = s_vo[row * kTileX + lane];
-      A.labels[gv + lane] = s_lab[row * kTileX + lane];
+  const int yy = y_t + warp;
+  if (yy < ny) {
+    const int zend = min(kTileZ, nz - z_t);
+    int64_t gv = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
+    const int64_t zstep = (int64_t)nx * ny;
+    const int nel = xw * C;
+    for (int zl = 0; zl < zend; ++zl, gv += zstep) {
+      const int row = zl * kTileY + warp;
+      if (A.v_c) {
+        const float* src = s_vc + row * kTileX * C;
+        float* dst = A.v_c + gv * C;
+        for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+      }
+      if (lane < xw) {
+        if (A.v_o) A.v_o[gv + lane] = s_vo[row * kTileX + lane];
+        A.labels[gv + lane] = s_lab[row * kTileX + lane];
+      }
     }
   }
 }

@@ -51,6 +51,7 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
 // primitives far from their centre voxel.
+template <bool EXACT_STEP>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords& cd) {
   const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
@@ -68,9 +69,15 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
 #pragma unroll
   for (int v = 1; v < kVPT; ++v) {
     const float fv = (float)v;
-    cd.p0[v] = fmaf(fv, R.H[2], h0) + fmaf(fv, R.L[2], l0);
-    cd.p1[v] = fmaf(fv, R.H[5], h1) + fmaf(fv, R.L[5], l1);
-    cd.p2[v] = fmaf(fv, R.H[8], h2) + fmaf(fv, R.L[8], l2);
+    if (EXACT_STEP) {  // strict: hi/lo stepping, exact
+      cd.p0[v] = fmaf(fv, R.H[2], h0) + fmaf(fv, R.L[2], l0);
+      cd.p1[v] = fmaf(fv, R.H[5], h1) + fmaf(fv, R.L[5], l1);
+      cd.p2[v] = fmaf(fv, R.H[8], h2) + fmaf(fv, R.L[8], l2);
+    } else {  // fast: <= 3 steps of the once-rounded z step (error <= 3 ulp(dz))
+      cd.p0[v] = fmaf(fv, R.Ez[0], cd.p0[0]);
+      cd.p1[v] = fmaf(fv, R.Ez[1], cd.p1[0]);
+      cd.p2[v] = fmaf(fv, R.Ez[2], cd.p2[0]);
+    }
   }
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
@@ -135,7 +142,7 @@ template <int FIELD>
 __device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int z0,
                                              float (&w)[kVPT]) {
   ColCoords cd;
-  pair_coords(R, x, y, z0, cd);
+  pair_coords<FIELD == 6>(R, x, y, z0, cd);
   pair_field<FIELD>(R, cd, w);
 }
 

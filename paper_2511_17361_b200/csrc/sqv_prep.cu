@@ -117,6 +117,7 @@ __global__ void prep_kernel(PrepArgs A) {
           const double row[3] = {P.M[3 * r2] * res, P.M[3 * r2 + 1] * res, P.M[3 * r2 + 2] * res};
           const double g = P.M[3 * r2] * d[0] + P.M[3 * r2 + 1] * d[1] + P.M[3 * r2 + 2] * d[2];
           split_row(row, g, &rec.H[3 * r2], &rec.L[3 * r2], &rec.Gh[r2], &rec.Gl[r2]);
+          rec.Ez[r2] = (float)row[2];
         }
         rec.a = (float)(2.0 / P.e2);
         rec.b = (float)(P.e2 / P.e1);

@@ -80,8 +80,8 @@ class VoxelizeConfig:
     semantic_mode ("logit-sum" | "prob-sum").  window_extent is the ledger's
     max-K expansion factor (default 2.5).  precision selects the
     device numerics: "strict" (default; densities within 1e-5 relative down to
-    1e-3*tau) or "fast" (all logs on the SFU, ~11% faster; 1e-5 relative for
-    v_o >= tau/10) — see DESIGN.md §Numerics."""
+    1e-3*tau) or "fast" (all logs on the SFU, ~13% faster; 2e-5 relative down to
+    1e-3*tau) — see DESIGN.md §Numerics."""
 
     tau: float = 0.01
     neighborhood_radius: int = 5

@@ -4,13 +4,11 @@
 * densities:
     precision="strict" (default):
     |v_o - ref| <= 1e-5 * max(ref, 1e-3*tau)   1e-5 relative down to 1e-3*tau;
-    precision="fast", two tiers:
-    |v_o - ref| <= 1e-5 * max(ref, tau/10)     every voxel that can decide a
-                                               label (v_o >= tau/10);
-    |v_o - ref| <= 2e-5 * max(ref, 1e-3*tau)   far-below-threshold tails (the
-                                               SFU log2 error, 2^-22 absolute,
-                                               is amplified by 2/eps1 <= 10 in F
-                                               and by F in exp(-F));
+    precision="fast":
+    |v_o - ref| <= 2e-5 * max(ref, 1e-3*tau)   (the SFU log2 error, 2^-22
+                                               absolute, is amplified by
+                                               2/eps1 <= 10 in F and by F in
+                                               exp(-F); z steps are rounded once);
 * labels: a voxel may disagree only where the oracle's top-2 class scores
   differ by < LABEL_GAP * max(1, |top-1|), or where the oracle's v_o lies
   within VO_REL of tau (a tau flip); overall agreement >= 99.99%.
@@ -19,9 +17,8 @@ from __future__ import annotations
 
 import numpy as np
 
-VO_REL = 1e-5
-VO_FLOOR_FRAC_TAU = 1e-1     # tier 1 floor: tau/10
-VO_REL_TAIL = 2e-5
+VO_REL = 1e-5                # strict
+VO_REL_TAIL = 2e-5           # fast
 VO_TAIL_FLOOR_FRAC_TAU = 1e-3
 LABEL_GAP = 1e-5
 MIN_AGREEMENT = 0.9999
@@ -35,8 +32,7 @@ def vo_check(gpu, ref, tau, mode="strict"):
     bad = np.zeros(err.shape, bool)
     tail_floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, 1e-9)
     tiers = ((("tier1", VO_REL, tail_floor),) if mode == "strict" else
-             (("tier1", VO_REL, max(VO_FLOOR_FRAC_TAU * tau, 1e-7)),
-              ("tail", VO_REL_TAIL, tail_floor)))
+             (("tier1", VO_REL_TAIL, tail_floor),))
     for name, rel, floor in tiers:
         scaled = err / np.maximum(ref, floor)
         out[f"worst_rel_{name}"] = float(scaled.max()) if err.size else 0.0

@@ -114,9 +114,9 @@ def test_config1_occ3d_256():
     print("config1 worst v_o rel", vo["worst_rel"], "label agreement", lab["agreement"])
 
 
-def test_fast_precision_mode_two_tier():
+def test_fast_precision_mode():
     """precision="fast" (all logs on the SFU): labels unchanged, densities within
-    the two-tier criterion."""
+    2e-5 relative down to 1e-3*tau."""
     P = _pkg()
     spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig(precision="fast")
     b = _scene(11, 256)
