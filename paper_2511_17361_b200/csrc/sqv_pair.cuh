@@ -54,7 +54,8 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
 template <bool EXACT_STEP>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords& cd) {
-  const bool in_xy = x >= R.lo[0] && x <= R.hi[0] && y >= R.lo[1] && y <= R.hi[1];
+  // bitwise (not short-circuit) tests: no divergent branches on loaded bounds
+  const bool in_xy = (x >= R.lo[0]) & (x <= R.hi[0]) & (y >= R.lo[1]) & (y <= R.hi[1]);
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
   const float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fmaf(fx, R.H[0], R.Gh[0])));
   const float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fmaf(fx, R.H[3], R.Gh[1])));
@@ -82,7 +83,7 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
     const int z = z0 + v;
-    cd.live[v] = in_xy && z >= loz && z <= hiz;
+    cd.live[v] = in_xy & (z >= loz) & (z <= hiz);
   }
 }
 
@@ -117,9 +118,41 @@ __device__ __forceinline__ bool wants_acc(const PrimRec& R) {
   return FIELD == 6 && R.c > 3.0f;
 }
 
+// The log-sum-exp field written step by step across the 4 voxels of the
+// column, so the 4 independent chains are interleaved in program order (the
+// evaluator is latency-bound; this is the schedule we want from ptxas).
+template <bool ACC>
+__device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords& cd,
+                                             float (&w)[kVPT]) {
+  const float a = R.a, b = R.b, c = R.c;
+  float ux[kVPT], uy[kVPT], uz[kVPT], um[kVPT], t[kVPT], F[kVPT];
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) {
+    ux[v] = a * (ACC ? log2_acc(fabsf(cd.p0[v])) : lg2(fabsf(cd.p0[v])));
+    uy[v] = a * (ACC ? log2_acc(fabsf(cd.p1[v])) : lg2(fabsf(cd.p1[v])));
+    uz[v] = c * (ACC ? log2_acc(fabsf(cd.p2[v])) : lg2(fabsf(cd.p2[v])));
+  }
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) {
+    um[v] = fmaxf(ux[v], uy[v]);
+    t[v] = ex2(fmaxf(fminf(ux[v], uy[v]) - um[v], -126.0f));
+  }
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) t[v] = log2_1p_poly(t[v]);
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) F[v] = ex2(b * (um[v] + t[v])) + ex2(uz[v]);
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v)
+    w[v] = (cd.live[v] & (F[v] < kFCut)) ? ex2(-F[v] * kLog2e) : 0.0f;
+}
+
 template <int FIELD, bool ACC>
 __device__ __forceinline__ void weights_one(const PrimRec& R, const ColCoords& cd,
                                             float (&w)[kVPT]) {
+  if (FIELD == 6 || FIELD == 7) {
+    weights_lse4<ACC>(R, cd, w);
+    return;
+  }
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
     const float F = field_of<FIELD, ACC>(cd.p0[v], cd.p1[v], cd.p2[v], R.a, R.b, R.c);
