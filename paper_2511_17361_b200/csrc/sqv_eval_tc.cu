@@ -283,12 +283,20 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     int64_t gv = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
     const int64_t zstep = (int64_t)nx * ny;
     const int nel = xw * C;
+    const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
+    const int nel4 = nel >> 2;
     for (int zl = 0; zl < zend; ++zl, gv += zstep) {
       const int row = zl * kTileY + warp;
       if (A.v_c) {
-        const float* src = s_vc + row * kTileX * C;
+        const float* src = s_vc + row * kTileX * C;  // 16-byte aligned: row*8*C*4
         float* dst = A.v_c + gv * C;
-        for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+        if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          const float4* s4 = reinterpret_cast<const float4*>(src);
+          float4* d4 = reinterpret_cast<float4*>(dst);
+          for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
+        } else {
+          for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+        }
       }
       if (lane < xw) {
         if (A.v_o) A.v_o[gv + lane] = s_vo[row * kTileX + lane];
