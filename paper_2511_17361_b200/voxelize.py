@@ -412,3 +412,38 @@ def finalize(dense: DenseGrids, tau: float, classes: ClassTable) -> SemanticGrid
     lab_h = labels_to_host(lab.cpu().numpy(), code, classes.free_index)
     spec = VoxelGridSpec(dims=shape)
     return SemanticGrid(_logical(lab_h), spec, classes)
+
+
+def truncation_report(batch: PrimitiveBatch, spec: VoxelGridSpec = VoxelGridSpec(),
+                      cfg: VoxelizeConfig = VoxelizeConfig()) -> dict:
+    """Truncated voxelize vs voxelize_bruteforce on the device (SPEC.md:376,
+    cmd_voxelize --oracle, SPEC.md:580).
+
+    Returns the max |dv_o| (omitted mass), the label mismatch rate, whether
+    every mismatching voxel lost positive mass (truncation soundness), and a
+    per-primitive tail bound: outside its window a primitive's local scaled
+    coordinates satisfy |x'|_inf >= (r - 1/2) res / (sqrt(3) max(s)), so
+    sigma * exp(-F) <= sigma * exp(-((r - 1/2) res / (sqrt(3) max(s)))^(2/eps1)).
+    """
+    import torch
+    C = batch.n_classes
+    tr = Voxelizer(spec, cfg, C, truncate=True)(batch)
+    bf = Voxelizer(spec, cfg, C, truncate=False)(batch)
+    dvo = (bf.v_o.double() - tr.v_o.double())
+    diff = tr.labels != bf.labels
+    sound = bool(torch.all(dvo[diff] > 0).item()) if bool(diff.any()) else True
+    sc = np.asarray(batch.scale, np.float64)
+    e1 = np.clip(np.asarray(batch.eps, np.float64)[..., 0], 0.2, 2.0)
+    smax = sc.max(-1)
+    r = cfg.neighborhood_radius + np.ceil(smax * cfg.window_extent / spec.resolution)
+    reach = np.maximum(r - 0.5, 0.0) * spec.resolution / (np.sqrt(3.0) * smax)
+    tail = np.asarray(batch.opacity, np.float64) * np.exp(-np.power(reach, 2.0 / e1))
+    if batch.n_valid is not None:
+        nv = np.asarray(batch.n_valid)
+        tail = np.where(np.arange(tail.shape[1])[None, :] < nv[:, None], tail, 0.0)
+    return {"max_omitted_mass": float(dvo.max().item()),
+            "min_dvo": float(dvo.min().item()),
+            "label_mismatch_rate": float(diff.double().mean().item()),
+            "sound": sound,
+            "max_single_primitive_tail_bound": float(tail.max()),
+            "sum_tail_bound": float(tail.sum(-1).max())}

@@ -323,3 +323,19 @@ def test_stream_api_matches_direct_calls():
     for b, lab in zip(batches, labels):
         direct = vox(b).labels.cpu()
         assert torch.equal(direct, lab)
+
+
+def test_truncation_report_soundness():
+    """cmd_voxelize --oracle: omitted mass is non-negative,
+    every label flip lost mass, and the omitted mass stays under the summed
+    per-primitive tail bound."""
+    P = _pkg()
+    from paper_2511_17361_b200.voxelize import truncation_report
+    spec = P.VoxelGridSpec((-6.4, -6.4, -6.4), (32, 32, 32), 0.4)
+    b = _scene(77, 40, C=8, origin=spec.origin, dims=spec.dims, resolution=spec.resolution,
+               smax=1.5)
+    rep = truncation_report(b, spec, P.VoxelizeConfig())
+    assert rep["sound"]
+    assert rep["min_dvo"] >= -1e-6
+    assert rep["max_omitted_mass"] <= rep["sum_tail_bound"] * (1 + 1e-4) + 1e-6
+    print(rep)
