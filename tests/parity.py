@@ -72,10 +72,13 @@ def assert_parity(gpu, ref, tau, free_code, check_vc=True, mode="strict"):
     assert lab["n_unexplained"] == 0, f"unexplained label mismatches: {lab}"
     assert lab["agreement"] >= MIN_AGREEMENT, lab
     if check_vc:
-        # class weights: absolute error relative to the voxel's weight scale
+        # class weights: absolute error relative to the voxel's weight scale,
+        # max(|v_c|, v_o) — v_o = sum(sigma w) bounds sum(w) from below, so it
+        # stands for the term magnitude when mixed-sign logits cancel in v_c
         vc_g = np.asarray(gpu["v_c"], np.float64)
         vc_r = np.asarray(ref["v_c"], np.float64)
-        scale = np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), 1e-3)
+        vo_r = np.asarray(ref["v_o"], np.float64).reshape(vc_r.shape[:-1] + (1,))
+        scale = np.maximum(np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), vo_r), 1e-3)
         rel = np.abs(vc_g - vc_r) / scale
         assert float(rel.max(initial=0.0)) <= 1e-4, f"v_c worst {float(rel.max())}"
     return vo, lab

@@ -339,3 +339,29 @@ def test_truncation_report_soundness():
     assert rep["min_dvo"] >= -1e-6
     assert rep["max_omitted_mass"] <= rep["sum_tail_bound"] * (1 + 1e-4) + 1e-6
     print(rep)
+
+
+@pytest.mark.parametrize("C", [1, 3, 24, 32])
+def test_class_counts(C):
+    """Every evaluator instantiation: C <= 24 runs on tcgen05, C = 32 on the
+    CUDA-core evaluator (sigma does not fit the N = 32 tensor-core tile)."""
+    P = _pkg()
+    spec = P.VoxelGridSpec((-8.0, -8.0, -2.0), (40, 40, 16), 0.4)
+    cfg = P.VoxelizeConfig()
+    b = _scene(90 + C, 150, C=C, origin=spec.origin, dims=spec.dims, smax=2.0)
+    out = _run(b, spec, cfg, C)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"])
+    assert_parity(out, ref, cfg.tau, out["free_code"])
+
+
+def test_ffma_and_tensor_core_evaluators_agree(monkeypatch):
+    """SQV_EVAL=ffma (CUDA-core accumulation) vs the default tcgen05 path."""
+    P = _pkg()
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    b = _scene(13, 400)
+    tc_out = _run(b, spec, cfg, 18)
+    monkeypatch.setenv("SQV_EVAL", "ffma")
+    ff_out = _run(b, spec, cfg, 18)
+    assert np.mean(tc_out["labels"] == ff_out["labels"]) > 0.99999
+    # 3xTF32 products (~2^-21 relative each) vs FP32 FFMA (2^-24)
+    np.testing.assert_allclose(tc_out["v_o"], ff_out["v_o"], rtol=5e-6, atol=1e-9)
