@@ -44,25 +44,52 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--frames-per-step", type=int, default=100)
-    ap.add_argument("--n-prims", type=int, default=2000)
+    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4], default=2,
+                    help="BASELINE.json configs: 1 = 256 SQs, 2 = 2k SQs (headline), "
+                         "3 = 4k SQs with eps in [0.1, 2], 4 = 8k SQs on 400x400x32 @0.2 m")
+    ap.add_argument("--frames-per-step", type=int, default=None)
+    ap.add_argument("--n-prims", type=int, default=None)
     ap.add_argument("--classes", type=int, default=18)
+    ap.add_argument("--precision", choices=["strict", "fast"], default="strict")
     ap.add_argument("--seed", type=int, default=20251117)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    w = WORKLOADS[a.config]
+    a.n_prims = a.n_prims or w["n_prims"]
+    a.frames_per_step = a.frames_per_step or w["frames_per_step"]
+    a.grid = dict(origin=w["origin"], dims=w["dims"], resolution=w["resolution"])
+    a.gen = dict(a.grid, emin=w["emin"])
+    return a
+
+
+WORKLOADS = {
+    1: dict(n_prims=256, frames_per_step=100, origin=(-40.0, -40.0, -1.0), dims=(200, 200, 16),
+            resolution=0.4, emin=0.2),
+    2: dict(n_prims=2000, frames_per_step=100, origin=(-40.0, -40.0, -1.0), dims=(200, 200, 16),
+            resolution=0.4, emin=0.2),
+    3: dict(n_prims=4000, frames_per_step=50, origin=(-40.0, -40.0, -1.0), dims=(200, 200, 16),
+            resolution=0.4, emin=0.1),
+    4: dict(n_prims=8000, frames_per_step=10, origin=(-40.0, -40.0, -1.0), dims=(400, 400, 32),
+            resolution=0.2, emin=0.2),
+}
 
 
 def workload_config(a, world):
-    return {"workload": f"config2: synthetic frames x {a.n_prims} SQs, Occ3D 200x200x16 @0.4 m, "
-                        f"{a.classes} classes, tau 0.01, N=5 window, logit-sum",
+    d = a.grid["dims"]
+    return {"workload": f"config{a.config}: synthetic frames x {a.n_prims} SQs, grid "
+                        f"{d[0]}x{d[1]}x{d[2]} @{a.grid['resolution']} m, {a.classes} classes, "
+                        f"tau 0.01, N=5 window, logit-sum, precision {a.precision}",
             "frames_per_step": a.frames_per_step, "frames_per_rank": a.frames_per_step * a.steps,
-            "n_prims": a.n_prims, "grid": [200, 200, 16], "resolution": 0.4,
+            "n_prims": a.n_prims, "grid": list(d), "resolution": a.grid["resolution"],
             "classes": a.classes, "generator": "scenegen.gen_frames (SPEC.md:594-597), seed "
-                                               f"{a.seed}+frame; s~U[0.2,4], eps~U[0.2,2]",
+                                               f"{a.seed}+frame; s~U[0.2,4], "
+                                               f"eps~U[{a.gen['emin']},2]",
             "outputs": "labels u8 + v_o f32 + v_c f32 written per frame; confusion vs gt",
-            "l2": "not flushed explicitly: each step writes ~4.9 GB of outputs (>> 126 MB L2)",
+            "l2": "not flushed explicitly: each step writes "
+                  f"{a.frames_per_step * d[0] * d[1] * d[2] * (5 + 4 * a.classes) / 1e9:.1f} GB "
+                  "of outputs (>> 126 MB L2)",
             "parallelism": f"frame-sharded x{world} (no data-path collective; int64 confusion "
                            "all-reduce over NCCL)"}
 
@@ -138,10 +165,10 @@ def cpu_run(a, max_frames, budget_s):
     from paper_2511_17361_b200.scenegen import gen_frames
     O.build()
     threads = O.threads()
-    grid, cfg = O.Grid(), O.Cfg()
+    grid, cfg = O.Grid(**a.grid), O.Cfg()
     done, pairs, t_total = 0, 0, 0.0
     while done < max_frames and (t_total < budget_s or done == 0):
-        b = O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=done))
+        b = O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=done, **a.gen))
         t0 = time.perf_counter()
         r = O.voxelize(b, grid, cfg)
         t_total += time.perf_counter() - t0
@@ -156,8 +183,8 @@ def run_reference(a, rank, world):
     from paper_2511_17361_b200.scenegen import gen_frames
     from oracle import oracle as O
     O.build()
-    grid, cfg = O.Grid(), O.Cfg()
-    frames = [O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=k))
+    grid, cfg = O.Grid(**a.grid), O.Cfg()
+    frames = [O.Prims.of(gen_frames(a.seed, 1, a.n_prims, a.classes, first_frame=k, **a.gen))
               for k in range(a.warmup + a.steps)]
     for k in range(a.warmup):
         O.voxelize(frames[k], grid, cfg)
@@ -198,14 +225,15 @@ def run_ours(a, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    spec = P.VoxelGridSpec(**a.grid)
+    cfg = P.VoxelizeConfig(precision=a.precision)
     C, B, K, W = a.classes, a.frames_per_step, a.steps, a.warmup
     vox = P.Voxelizer(spec, cfg, C)
     n_batches = K
     first = rank * n_batches * B  # disjoint frames per rank (weak scaling)
 
     # ---- synthetic inputs (host, seeded) + ground truth (untimed) ----
-    host_batches = [gen_frames(a.seed, B, a.n_prims, C, first_frame=first + k * B)
+    host_batches = [gen_frames(a.seed, B, a.n_prims, C, first_frame=first + k * B, **a.gen)
                     for k in range(n_batches)]
     dev_batches = [vox.to_device(b) for b in host_batches]
     gt = []
