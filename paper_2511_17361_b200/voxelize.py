@@ -279,6 +279,28 @@ class Voxelizer:
         t = self.torch
         if batch.n_classes != self.C:
             raise ValueError(f"batch has {batch.n_classes} classes, voxelizer expects {self.C}")
+        with t.cuda.device(self.device):
+            try:
+                return self._run(batch, dense, bins, out)
+            except _lib.SqvError as e:
+                # index spaces are 32-bit per call: halve the frames and retry
+                if "split frames" not in str(e) or batch.n_frames < 2 or bins:
+                    raise
+            F, h = batch.n_frames, batch.n_frames // 2
+            if out is None:
+                out = self.alloc(F, dense)
+            part = lambda a, lo, hi: None if a is None else a[lo:hi]
+            rs = [self(batch.frames(lo, hi), dense=dense,
+                       out=VoxelizeResult(out.labels[lo:hi], part(out.v_o, lo, hi),
+                                          part(out.v_c, lo, hi)))
+                  for lo, hi in ((0, h), (h, F))]
+            out.free_code = self.free_code
+            out.n_pairs = sum(r.n_pairs for r in rs)
+            out.n_entries = sum(r.n_entries for r in rs)
+            return out
+
+    def _run(self, batch, dense, bins, out):
+        t = self.torch
         db = self.to_device(batch)
         F, N = db.n_frames, db.n_prims
         if out is None:

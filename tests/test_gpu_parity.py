@@ -365,3 +365,23 @@ def test_ffma_and_tensor_core_evaluators_agree(monkeypatch):
     assert np.mean(tc_out["labels"] == ff_out["labels"]) > 0.99999
     # 3xTF32 products (~2^-21 relative each) vs FP32 FFMA (2^-24)
     np.testing.assert_allclose(tc_out["v_o"], ff_out["v_o"], rtol=5e-6, atol=1e-9)
+
+
+def test_degenerate_inputs_and_free_index():
+    """N = 0 primitives, tau = inf, and a free_index outside a byte."""
+    P = _pkg()
+    spec = P.VoxelGridSpec((-2.0, -2.0, -2.0), (9, 7, 5), 0.5)
+    z = lambda *s: np.zeros(s)
+    empty = P.PrimitiveBatch(z(2, 0, 3), z(2, 0, 3), z(2, 0, 4), z(2, 0), z(2, 0, 2), z(2, 0, 3))
+    r = P.Voxelizer(spec, P.VoxelizeConfig(), 3)(empty)
+    assert r.n_pairs == 0 and bool((r.labels == r.free_code).all()) and float(r.v_o.abs().max()) == 0
+    b = _scene(8, 30, C=3, origin=spec.origin, dims=spec.dims, resolution=spec.resolution, smax=1.0)
+    r = P.Voxelizer(spec, P.VoxelizeConfig(tau=float("inf")), 3)(b)
+    assert bool((r.labels == r.free_code).all())
+    classes = P.ClassTable(("a", "b", "c"), free_index=-1)
+    prims = [P.SuperQuadric(mu=[0, 0, 0], scale=[1, 1, 1], rot=[1, 0, 0, 0], opacity=1.0,
+                            logits=[0.0, 2.0, 1.0], eps1=1.0, eps2=1.0)]
+    sem, dense = P.voxelize(P.Scene(prims, classes), spec)
+    lab = np.asarray(sem.labels)
+    assert lab.min() == -1 and set(np.unique(lab)) <= {-1, 1}
+    assert lab[4, 4, 2] == 1
