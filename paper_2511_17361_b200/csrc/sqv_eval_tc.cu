@@ -56,7 +56,9 @@ struct TcShape {
   static constexpr int kBar = (kMask + kWarps * kMaskWords * 4 + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
   static constexpr int kEnd = kMisc + 4 + kWarps * 4;
-  static constexpr int kStage = 1024 * (CM * 4 + 4 + 1);  // epilogue staging (aliases kA..)
+  // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
+  // holding z-adjacent voxels hit different banks
+  static constexpr int kStage = 16 * ((64 * CM + 8) * 4 + 72 * 4 + 72);
   static constexpr int kBody = kEnd > kStage ? kEnd : kStage;
   static constexpr int kSmem = kBody + 1024;               // + alignment slack
   static_assert(kSmem <= 113 * 1024, "two CTAs per SM");
@@ -230,9 +232,11 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   const int C = A.n_classes;
   const int nx = A.nx, ny = A.ny, nz = A.nz;
   const int x_t = tx * kTileX, y_t = ty * kTileY, z_t = tz * kTileZ;
-  float* s_vc = reinterpret_cast<float*>(smem);        // [1024][C]
-  float* s_vo = s_vc + 1024 * C;                       // [1024]
-  uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 1024);
+  const int zpc = 64 * C + 8;                          // padded z pitches
+  constexpr int zpo = 72;
+  float* s_vc = reinterpret_cast<float*>(smem);        // [16][zpc]
+  float* s_vo = s_vc + 16 * zpc;                       // [16][zpo]
+  uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 16 * zpo);
   const int qd = warp & 3;  // TMEM lane quarter this warp may access
 #pragma unroll 1
   for (int i = 0; i < 4; ++i) {
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     const int vx = (mb & 1) * 4 + (src & 3);
     const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
     const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
-    const int loc = vx + kTileX * (vy + kTileY * vz);
+    const int loc = vx + kTileX * vy;  // within the z layer
     int best = 0;
     float bv = vals[0];
 #pragma unroll
@@ -262,10 +266,10 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     if (A.v_c) {
 #pragma unroll
       for (int k = 0; k < CM; ++k)
-        if (k < C) s_vc[loc * C + k] = vals[k];
+        if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
     }
-    s_vo[loc] = vo;
-    s_lab[loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
+    s_vo[vz * zpo + loc] = vo;
+    s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     for (int zl = 0; zl < zend; ++zl, gv += zstep) {
       const int row = zl * kTileY + warp;
       if (A.v_c) {
-        const float* src = s_vc + row * kTileX * C;  // 16-byte aligned: row*8*C*4
+        const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
         float* dst = A.v_c + gv * C;
         if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
           const float4* s4 = reinterpret_cast<const float4*>(src);
@@ -299,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         }
       }
       if (lane < xw) {
-        if (A.v_o) A.v_o[gv + lane] = s_vo[row * kTileX + lane];
-        A.labels[gv + lane] = s_lab[row * kTileX + lane];
+        if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
+        A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
       }
     }
   }
