@@ -29,6 +29,8 @@
 #include "sqv_pair.cuh"
 #include "sqv_tc.cuh"
 
+#include <type_traits>
+
 namespace sqv {
 
 namespace {
@@ -36,7 +38,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = 8;
 constexpr int kMaxChunk = 128;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
-constexpr int kMaskWords = kMaxChunk / 32;
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
 constexpr int kN = 32;       // class weights + sigma, padded
 constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
@@ -52,8 +53,10 @@ struct TcShape {
   static constexpr int kB = kA + kWarps * 2 * 4096;
   static constexpr int kRec = kB + kWarps * 2 * 1024;
   static constexpr int kLw = kRec + kChunk * kRecWords * 4;
-  static constexpr int kMask = kLw + kChunk * kLRow * 4;
-  static constexpr int kBar = (kMask + kWarps * kMaskWords * 4 + 7) & ~7;
+  // per-warp hit lists (chunk-local primitive indices, u8): primitives whose
+  // window covers the warp's whole block from the front, the rest from the back
+  static constexpr int kList = kLw + kChunk * kLRow * 4;
+  static constexpr int kBar = (kList + kWarps * kChunk + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
   static constexpr int kEnd = kMisc + 4 + kWarps * 4;
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   float* s_rec = reinterpret_cast<float*>(smem + S::kRec);
   float* s_lw = reinterpret_cast<float*>(smem + S::kLw);
-  unsigned* s_mask = reinterpret_cast<unsigned*>(smem + S::kMask);
+  uint8_t* s_list = smem + S::kList;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
@@ -134,13 +137,14 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   // primitive in K slot k: A rows lane*4 + v (one STS.128), B row lane
   // per-lane parts of the operand offsets (tc::mn32_offset with mn = lane*4
   // for A, mn = lane for B); the K slot adds a uniform part and a swizzle XOR
-  const uint32_t a_base = (uint32_t)((lane >> 3) * 512 + (lane & 1) * 16);
-  const uint32_t a_t = (uint32_t)(((lane >> 1) & 3) << 5);
-  const uint32_t b_base = (uint32_t)((lane & 7) * 4);
-  const uint32_t b_t = (uint32_t)(((lane >> 3) & 3) << 5);
+  // The lane parts (bits 2-6, 9-10) and the K-slot parts (bits 7-8, 9 or 11)
+  // occupy disjoint bits except the swizzle bits 5-6, so offset = lane ^ slot.
+  const uint32_t a_lane = (uint32_t)((lane >> 3) * 512 + (lane & 1) * 16) |
+                          (uint32_t)(((lane >> 1) & 3) << 5);
+  const uint32_t b_lane = (uint32_t)((lane & 7) * 4) | (uint32_t)(((lane >> 3) & 3) << 5);
   auto store_k = [&](int k, const float(&w)[kVPT], float cw) {
-    const uint32_t kq = (uint32_t)(k & 3), kh = (uint32_t)(k >> 2), kx = kq << 5;
-    const uint32_t ao = a_base + kh * 2048u + kq * 128u + (a_t ^ kx);
+    const uint32_t kq = (uint32_t)(k & 3) * 160u, kh = (uint32_t)(k & 4);
+    const uint32_t ao = a_lane ^ (kq | (kh << 9));
     float4 h, l;
     h.x = tf32_hi(w[0]);
     h.y = tf32_hi(w[1]);
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     l.w = w[3] - h.w;
     *reinterpret_cast<float4*>(a_hi + ao) = h;
     *reinterpret_cast<float4*>(a_lo + ao) = l;
-    const uint32_t bo = b_base + kh * 512u + kq * 128u + (b_t ^ kx);
+    const uint32_t bo = b_lane ^ (kq | (kh << 7));
     const float ch = tf32_hi(cw);
     *reinterpret_cast<float*>(b_hi + bo) = ch;
     *reinterpret_cast<float*>(b_lo + bo) = cw - ch;
@@ -190,32 +194,39 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + q);
     }
     __syncthreads();
+    uint8_t* lst = s_list + warp * S::kChunk;
+    int n_in = 0, n_part = 0;  // warp-uniform list lengths
+    const unsigned lt = (1u << lane) - 1u;
     for (int q = 0; q * 32 < n; ++q) {
       const int j = q * 32 + lane;
-      bool hit = false;
+      bool hit = false, inside = false;
       if (j < n) {
-        hit = block_may_hit(*reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords), bx0, by0,
-                            bz0);
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        hit = block_may_hit(R, bx0, by0, bz0);
+        inside = hit && block_inside(R, bx0, by0, bz0);
       }
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) s_mask[warp * kMaskWords + q] = m;
+      const unsigned mi = __ballot_sync(0xffffffffu, inside);
+      const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
+      if (inside) lst[n_in + __popc(mi & lt)] = (uint8_t)j;
+      if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = (uint8_t)j;
+      n_in += __popc(mi);
+      n_part += __popc(mp);
     }
     __syncwarp();
-    for (int q = 0; q * 32 < n; ++q) {
-      unsigned m = s_mask[warp * kMaskWords + q];
-      while (m) {
-        const int j = q * 32 + __ffs(m) - 1;
-        m &= m - 1;
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
-        float w[kVPT];
-        pair_weights<FIELD>(R, x, y, z0, w);
-        // class weight n = lane (sigma at CM), zero beyond
-        const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
-        if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
-        store_k(kk, w, cw);
-        if (++kk == kK) issue();
-      }
-    }
+    auto visit = [&](int j, auto live) {
+      const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+      float w[kVPT];
+      pair_weights<FIELD, decltype(live)::value>(R, x, y, z0, w);
+      // class weight n = lane (sigma at CM), zero beyond
+      const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
+      if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
+      store_k(kk, w, cw);
+      if (++kk == kK) issue();
+    };
+    // whole-block primitives first (no per-voxel window test), then the rest,
+    // each in ascending primitive order
+    for (int i = 0; i < n_in; ++i) visit(lst[i], std::false_type{});
+    for (int i = 0; i < n_part; ++i) visit(lst[S::kChunk - 1 - i], std::true_type{});
   }
   if (kk > 0) {  // close the last K step with zero columns
     const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};

@@ -39,6 +39,13 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
   return dmax <= R.mcut + 1e-4f * slack;
 }
 
+// Is the warp's whole 4x4x8 block inside R's window?  Then no voxel of the
+// block needs the per-voxel window test (pair_coords<.., LIVE = false>).
+__device__ __forceinline__ bool block_inside(const PrimRec& R, int bx0, int by0, int bz0) {
+  return (bx0 >= R.lo[0]) & (bx0 + 3 <= R.hi[0]) & (by0 >= R.lo[1]) & (by0 + 3 <= R.hi[1]) &
+         (bz0 >= R.lo[2]) & (bz0 + 7 <= R.hi[2]);
+}
+
 // Coordinates + liveness of primitive R at voxels (x, y, z0 + v), v < 4.
 // The caller has already established — per warp, with block_may_hit — that
 // the primitive can reach the warp's block, so there is no further cull
@@ -51,7 +58,7 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
 // primitives far from their centre voxel.
-template <bool EXACT_STEP>
+template <bool EXACT_STEP, bool LIVE = true>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords& cd) {
   // bitwise (not short-circuit) tests: no divergent branches on loaded bounds
@@ -83,7 +90,7 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
     const int z = z0 + v;
-    cd.live[v] = in_xy & (z >= loz) & (z <= hiz);
+    cd.live[v] = LIVE ? (in_xy & (z >= loz) & (z <= hiz)) : true;
   }
 }
 
@@ -171,11 +178,11 @@ __device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords& cd
 }
 
 // Single-primitive convenience (coords + field).
-template <int FIELD>
+template <int FIELD, bool LIVE = true>
 __device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int z0,
                                              float (&w)[kVPT]) {
   ColCoords cd;
-  pair_coords<FIELD == 6>(R, x, y, z0, cd);
+  pair_coords<FIELD == 6, LIVE>(R, x, y, z0, cd);
   pair_field<FIELD>(R, cd, w);
 }
 
