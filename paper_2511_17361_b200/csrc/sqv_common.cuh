@@ -26,9 +26,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
 
 // Per-primitive evaluation record (FP32, 40 words = 10 x float4).
-//   H[r][j], L[r][j]: hi/lo split of res * M'[r][j], M' = diag(1/s) * Rwl
-//   Gh[r], Gl[r]:     hi/lo split (same row quantum as H) of the local
-//                     (scaled) coords of the reference voxel centre
+//   HL[3r+j]:         (hi, lo) split of res * M'[r][j], M' = diag(1/s) * Rwl
+//   G[r]:             (hi, lo) split (same row quantum) of the local (scaled)
+//                     coords of the reference voxel centre
+//   (hi, lo) pairs are adjacent so one packed FFMA2 steps both)
 //   a, b, c:          2/eps2, eps2/eps1, 2/eps1 (core.py:267-269)
 //   mcut:             Chebyshev cull bound, F >= max|x'|^(2/eps1)
 //   cx, cy, cz:       reference voxel index (exact small integers)
@@ -37,10 +38,8 @@ constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
 // (sigma travels with the class weights, see prep's lrows.)
 constexpr int kRecWords = 40;
 struct __align__(16) PrimRec {
-  float H[9];
-  float L[9];
-  float Gh[3];
-  float Gl[3];
+  float2 HL[9];
+  float2 G[3];
   float a, b, c;
   float mcut;
   float cx, cy, cz;

@@ -8,13 +8,6 @@ namespace sqv {
 
 constexpr int kVPT = 4;  // voxels per thread: a 1x1x4 z-column
 
-// Local coordinates of a thread's 4 voxels for one primitive, and which of
-// them are live (inside the window and not culled).
-struct ColCoords {
-  float p0[kVPT], p1[kVPT], p2[kVPT];
-  bool live[kVPT];
-};
-
 // Can primitive R contribute to the warp's 4x4x8 voxel block at (bx0, by0,
 // bz0)?  Window overlap, then a conservative geometric test: the block's
 // centre in local coordinates minus its local half extent must come within
@@ -29,9 +22,9 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
   float dmax = -1.0f, slack = 0.0f;
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const float ex = R.H[3 * r] + R.L[3 * r], ey = R.H[3 * r + 1] + R.L[3 * r + 1],
-                ez = R.H[3 * r + 2] + R.L[3 * r + 2];
-    const float c = fmaf(kz, ez, fmaf(ky, ey, fmaf(kx, ex, R.Gh[r] + R.Gl[r])));
+    const float ex = R.HL[3 * r].x + R.HL[3 * r].y, ey = R.HL[3 * r + 1].x + R.HL[3 * r + 1].y,
+                ez = R.HL[3 * r + 2].x + R.HL[3 * r + 2].y;
+    const float c = fmaf(kz, ez, fmaf(ky, ey, fmaf(kx, ex, R.G[r].x + R.G[r].y)));
     const float h = 1.5f * fabsf(ex) + 1.5f * fabsf(ey) + 3.5f * fabsf(ez);
     dmax = fmaxf(dmax, fabsf(c) - h);
     slack += fabsf(c) + h;
@@ -46,52 +39,110 @@ __device__ __forceinline__ bool block_inside(const PrimRec& R, int bx0, int by0,
          (bz0 >= R.lo[2]) & (bz0 + 7 <= R.hi[2]);
 }
 
+// ---- packed FP32x2 helpers (FFMA2 / FADD2 / FMUL2: two lanes of work per
+// issue slot; same IEEE round-to-nearest results as the scalar ops) --------
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+// log2_1p_poly on a pair (same operations, same rounding).
+__device__ __forceinline__ float2 log2_1p_poly2(float2 t) {
+  const float2 t2 = mul2(t, t);
+  const float2 p01 = fma2(bc2(4.786837101e-01f), t, bc2(-7.211657763e-01f));
+  const float2 p23 = fma2(bc2(2.418647856e-01f), t, bc2(-3.473010957e-01f));
+  const float2 p45 = fma2(bc2(5.205900222e-02f), t, bc2(-1.375213563e-01f));
+  const float2 t4 = mul2(t2, t2);
+  const float2 q03 = fma2(p23, t2, p01);
+  const float2 q47 = fma2(bc2(-9.309163317e-03f), t2, p45);
+  const float2 q = fma2(q47, t4, q03);
+  return fma2(t, bc2(1.442689896e+00f), mul2(t2, q));
+}
+
+// log2_acc on a pair: the exponent split is integer work per lane, the
+// polynomial runs packed.
+__device__ __forceinline__ float2 log2_acc2(float2 x) {
+  const int i0 = __float_as_int(x.x), i1 = __float_as_int(x.y);
+  const int e0 = (i0 - 0x3f3504f3) >> 23, e1 = (i1 - 0x3f3504f3) >> 23;
+  const float2 r = add2(make_float2(__int_as_float(i0 - (e0 << 23)),
+                                    __int_as_float(i1 - (e1 << 23))), bc2(-1.0f));
+  float2 q = bc2(1.258370578e-01f);
+  q = fma2(q, r, bc2(-2.072697580e-01f));
+  q = fma2(q, r, bc2(2.157156020e-01f));
+  q = fma2(q, r, bc2(-2.389448136e-01f));
+  q = fma2(q, r, bc2(2.879162431e-01f));
+  q = fma2(q, r, bc2(-3.607036769e-01f));
+  q = fma2(q, r, bc2(4.809106290e-01f));
+  q = fma2(q, r, bc2(-7.213473320e-01f));
+  q = fma2(q, r, bc2(1.442695022e+00f));
+  const float2 l = fma2(r, q, make_float2((float)e0, (float)e1));
+  return make_float2(x.x >= 1.17549435e-38f ? l.x : -INFINITY,
+                     x.y >= 1.17549435e-38f ? l.y : -INFINITY);
+}
+
+// Local coordinates of a thread's 4 voxels, packed by voxel pairs:
+// P[r][h] = coordinate r of voxels (2h, 2h+1).
+struct ColCoords2 {
+  float2 P[3][2];
+  bool live[kVPT];
+};
+
 // Coordinates + liveness of primitive R at voxels (x, y, z0 + v), v < 4.
 // The caller has already established — per warp, with block_may_hit — that
 // the primitive can reach the warp's block, so there is no further cull
-// here: a voxel is live when it is inside the window; voxels with
-// F >= kFCut get w = 0 from the field itself (exactly what culling would
-// have produced).
+// here: a voxel is live when it is inside the window (LIVE = false: the
+// caller knows the whole block is); voxels with F >= kFCut get w = 0 from the
+// field itself (exactly what culling would have produced).
 //
 // Local coordinates use the exact lattice stepping of prep's split_row: the
 // hi parts (10 significant bits per row, the reference offset on the same
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
-// primitives far from their centre voxel.
+// primitives far from their centre voxel.  (hi, lo) run as one packed pair.
 template <bool EXACT_STEP, bool LIVE = true>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
-                                            ColCoords& cd) {
-  // bitwise (not short-circuit) tests: no divergent branches on loaded bounds
-  const bool in_xy = (x >= R.lo[0]) & (x <= R.hi[0]) & (y >= R.lo[1]) & (y <= R.hi[1]);
+                                            ColCoords2& cd) {
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
-  const float h0 = fmaf(fz, R.H[2], fmaf(fy, R.H[1], fmaf(fx, R.H[0], R.Gh[0])));
-  const float h1 = fmaf(fz, R.H[5], fmaf(fy, R.H[4], fmaf(fx, R.H[3], R.Gh[1])));
-  const float h2 = fmaf(fz, R.H[8], fmaf(fy, R.H[7], fmaf(fx, R.H[6], R.Gh[2])));
-  const float l0 = fmaf(fz, R.L[2], fmaf(fy, R.L[1], fmaf(fx, R.L[0], R.Gl[0])));
-  const float l1 = fmaf(fz, R.L[5], fmaf(fy, R.L[4], fmaf(fx, R.L[3], R.Gl[1])));
-  const float l2 = fmaf(fz, R.L[8], fmaf(fy, R.L[7], fmaf(fx, R.L[6], R.Gl[2])));
-  const int loz = R.lo[2], hiz = R.hi[2];
-  cd.p0[0] = h0 + l0;
-  cd.p1[0] = h1 + l1;
-  cd.p2[0] = h2 + l2;
+  const float2 v01 = make_float2(0.0f, 1.0f), v23 = make_float2(2.0f, 3.0f);
 #pragma unroll
-  for (int v = 1; v < kVPT; ++v) {
-    const float fv = (float)v;
+  for (int r = 0; r < 3; ++r) {
+    // (h, l) = (hi, lo) parts of coordinate r at voxel 0
+    const float2 hl =
+        fma2(bc2(fz), R.HL[3 * r + 2], fma2(bc2(fy), R.HL[3 * r + 1], fma2(bc2(fx), R.HL[3 * r], R.G[r])));
     if (EXACT_STEP) {  // strict: hi/lo stepping, exact
-      cd.p0[v] = fmaf(fv, R.H[2], h0) + fmaf(fv, R.L[2], l0);
-      cd.p1[v] = fmaf(fv, R.H[5], h1) + fmaf(fv, R.L[5], l1);
-      cd.p2[v] = fmaf(fv, R.H[8], h2) + fmaf(fv, R.L[8], l2);
+      const float2 h01 = fma2(v01, bc2(R.HL[3 * r + 2].x), bc2(hl.x));
+      const float2 h23 = fma2(v23, bc2(R.HL[3 * r + 2].x), bc2(hl.x));
+      const float2 l01 = fma2(v01, bc2(R.HL[3 * r + 2].y), bc2(hl.y));
+      const float2 l23 = fma2(v23, bc2(R.HL[3 * r + 2].y), bc2(hl.y));
+      cd.P[r][0] = add2(h01, l01);
+      cd.P[r][1] = add2(h23, l23);
     } else {  // fast: <= 3 steps of the once-rounded z step (error <= 3 ulp(dz))
-      cd.p0[v] = fmaf(fv, R.Ez[0], cd.p0[0]);
-      cd.p1[v] = fmaf(fv, R.Ez[1], cd.p1[0]);
-      cd.p2[v] = fmaf(fv, R.Ez[2], cd.p2[0]);
+      const float p0 = hl.x + hl.y;
+      cd.P[r][0] = fma2(v01, bc2(R.Ez[r]), bc2(p0));
+      cd.P[r][1] = fma2(v23, bc2(R.Ez[r]), bc2(p0));
     }
   }
+  if (LIVE) {
+    // bitwise (not short-circuit) tests: no divergent branches on loaded bounds
+    const bool in_xy = (x >= R.lo[0]) & (x <= R.hi[0]) & (y >= R.lo[1]) & (y <= R.hi[1]);
+    const int loz = R.lo[2], hiz = R.hi[2];
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) {
-    const int z = z0 + v;
-    cd.live[v] = LIVE ? (in_xy & (z >= loz) & (z <= hiz)) : true;
+    for (int v = 0; v < kVPT; ++v) {
+      const int z = z0 + v;
+      cd.live[v] = in_xy & (z >= loz) & (z <= hiz);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < kVPT; ++v) cd.live[v] = true;
   }
+}
+
+__device__ __forceinline__ float2 abs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+
+template <bool ACC>
+__device__ __forceinline__ float2 log2p(float2 a) {
+  if (ACC) return log2_acc2(abs2(a));
+  return make_float2(lg2(fabsf(a.x)), lg2(fabsf(a.y)));
 }
 
 // Field of one voxel with either SFU logs (ACC = false) or FMA-pipe ~1 ulp
@@ -125,36 +176,45 @@ __device__ __forceinline__ bool wants_acc(const PrimRec& R) {
   return FIELD == 6 && R.c > 3.0f;
 }
 
-// The log-sum-exp field written step by step across the 4 voxels of the
-// column, so the 4 independent chains are interleaved in program order (the
-// evaluator is latency-bound; this is the schedule we want from ptxas).
+// The log-sum-exp field of the column's 4 voxels as two packed voxel pairs:
+// the FMA-pipe work (scalings, the log2(1+t) polynomial, sums) issues once
+// per pair, the SFU work per voxel; the independent chains interleave.
 template <bool ACC>
-__device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords& cd,
+__device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords2& cd,
                                              float (&w)[kVPT]) {
   const float a = R.a, b = R.b, c = R.c;
-  float ux[kVPT], uy[kVPT], uz[kVPT], um[kVPT], t[kVPT], F[kVPT];
+  float2 ux[2], uy[2], uz[2], um[2], t[2], F[2];
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) {
-    ux[v] = a * (ACC ? log2_acc(fabsf(cd.p0[v])) : lg2(fabsf(cd.p0[v])));
-    uy[v] = a * (ACC ? log2_acc(fabsf(cd.p1[v])) : lg2(fabsf(cd.p1[v])));
-    uz[v] = c * (ACC ? log2_acc(fabsf(cd.p2[v])) : lg2(fabsf(cd.p2[v])));
+  for (int h = 0; h < 2; ++h) {
+    ux[h] = mul2(bc2(a), log2p<ACC>(cd.P[0][h]));
+    uy[h] = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
+    uz[h] = mul2(bc2(c), log2p<ACC>(cd.P[2][h]));
   }
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) {
-    um[v] = fmaxf(ux[v], uy[v]);
-    t[v] = ex2(fmaxf(fminf(ux[v], uy[v]) - um[v], -126.0f));
+  for (int h = 0; h < 2; ++h) {
+    um[h] = make_float2(fmaxf(ux[h].x, uy[h].x), fmaxf(ux[h].y, uy[h].y));
+    const float2 mn = make_float2(fminf(ux[h].x, uy[h].x), fminf(ux[h].y, uy[h].y));
+    const float2 d = add2(mn, make_float2(-um[h].x, -um[h].y));
+    t[h] = make_float2(ex2(fmaxf(d.x, -126.0f)), ex2(fmaxf(d.y, -126.0f)));
   }
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) t[v] = log2_1p_poly(t[v]);
+  for (int h = 0; h < 2; ++h) t[h] = log2_1p_poly2(t[h]);
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) F[v] = ex2(b * (um[v] + t[v])) + ex2(uz[v]);
+  for (int h = 0; h < 2; ++h) {
+    const float2 e = mul2(bc2(b), add2(um[h], t[h]));
+    F[h] = add2(make_float2(ex2(e.x), ex2(e.y)), make_float2(ex2(uz[h].x), ex2(uz[h].y)));
+  }
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v)
-    w[v] = (cd.live[v] & (F[v] < kFCut)) ? ex2(-F[v] * kLog2e) : 0.0f;
+  for (int h = 0; h < 2; ++h) {
+    const float2 arg = mul2(F[h], bc2(-kLog2e));
+    const float e0 = ex2(arg.x), e1 = ex2(arg.y);
+    w[2 * h] = (cd.live[2 * h] & (F[h].x < kFCut)) ? e0 : 0.0f;
+    w[2 * h + 1] = (cd.live[2 * h + 1] & (F[h].y < kFCut)) ? e1 : 0.0f;
+  }
 }
 
 template <int FIELD, bool ACC>
-__device__ __forceinline__ void weights_one(const PrimRec& R, const ColCoords& cd,
+__device__ __forceinline__ void weights_one(const PrimRec& R, const ColCoords2& cd,
                                             float (&w)[kVPT]) {
   if (FIELD == 6 || FIELD == 7) {
     weights_lse4<ACC>(R, cd, w);
@@ -162,14 +222,17 @@ __device__ __forceinline__ void weights_one(const PrimRec& R, const ColCoords& c
   }
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
-    const float F = field_of<FIELD, ACC>(cd.p0[v], cd.p1[v], cd.p2[v], R.a, R.b, R.c);
+    const float x0 = (v & 1) ? cd.P[0][v >> 1].y : cd.P[0][v >> 1].x;
+    const float x1 = (v & 1) ? cd.P[1][v >> 1].y : cd.P[1][v >> 1].x;
+    const float x2 = (v & 1) ? cd.P[2][v >> 1].y : cd.P[2][v >> 1].x;
+    const float F = field_of<FIELD, ACC>(x0, x1, x2, R.a, R.b, R.c);
     w[v] = (cd.live[v] && F < kFCut) ? ex2(-F * kLog2e) : 0.0f;
   }
 }
 
 // w = exp(-F) (0 for dead voxels) of one primitive.
 template <int FIELD>
-__device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords& cd,
+__device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords2& cd,
                                            float (&w)[kVPT]) {
   if (wants_acc<FIELD>(R))
     weights_one<FIELD, true>(R, cd, w);
@@ -181,7 +244,7 @@ __device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords& cd
 template <int FIELD, bool LIVE = true>
 __device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int z0,
                                              float (&w)[kVPT]) {
-  ColCoords cd;
+  ColCoords2 cd;
   pair_coords<FIELD == 6, LIVE>(R, x, y, z0, cd);
   pair_field<FIELD>(R, cd, w);
 }

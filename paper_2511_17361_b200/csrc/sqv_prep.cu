@@ -20,14 +20,12 @@ namespace sqv {
 // row is exact in FP32, so lattice offsets never cancel catastrophically.
 // The reference-voxel offset g of the row is split on the same quantum, so
 // g_hi + sum_j k_j * hi_j is an exact FP32 sum too.
-__device__ inline void split_row(const double v[3], double g, float hi[3], float lo[3],
-                                 float* g_hi, float* g_lo) {
+__device__ inline void split_row(const double v[3], double g, float2 hl[3], float2* gp) {
   const double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fabs(v[2]));
   if (m == 0.0) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) hi[j] = lo[j] = 0.0f;
-    *g_hi = 0.0f;
-    *g_lo = (float)g;
+    for (int j = 0; j < 3; ++j) hl[j] = make_float2(0.0f, 0.0f);
+    *gp = make_float2(0.0f, (float)g);
     return;
   }
   int e;
@@ -37,12 +35,12 @@ __device__ inline void split_row(const double v[3], double g, float hi[3], float
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     const double h = rint(v[j] * iq) * q;
-    hi[j] = (float)h;                 // exact: <= 11 significant bits
-    lo[j] = (float)(v[j] - h);
+    hl[j] = make_float2((float)h,     // exact: <= 11 significant bits
+                        (float)(v[j] - h));
   }
   const double gh = rint(g * iq) * q;
-  *g_hi = (float)gh;                  // exact while |g| < 2^(e+13)
-  *g_lo = (float)(g - gh);
+  *gp = make_float2((float)gh,        // exact while |g| < 2^(e+13)
+                    (float)(g - gh));
 }
 
 __global__ void prep_kernel(PrepArgs A) {
@@ -116,7 +114,7 @@ __global__ void prep_kernel(PrepArgs A) {
         for (int r2 = 0; r2 < 3; ++r2) {
           const double row[3] = {P.M[3 * r2] * res, P.M[3 * r2 + 1] * res, P.M[3 * r2 + 2] * res};
           const double g = P.M[3 * r2] * d[0] + P.M[3 * r2 + 1] * d[1] + P.M[3 * r2 + 2] * d[2];
-          split_row(row, g, &rec.H[3 * r2], &rec.L[3 * r2], &rec.Gh[r2], &rec.Gl[r2]);
+          split_row(row, g, &rec.HL[3 * r2], &rec.G[r2]);
           rec.Ez[r2] = (float)row[2];
         }
         rec.a = (float)(2.0 / P.e2);
