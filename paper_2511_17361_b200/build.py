@@ -50,7 +50,8 @@ def up_to_date() -> bool:
 
 def _compile(src: str, verbose: bool) -> tuple[str, str]:
     obj = os.path.join(OUT, os.path.basename(src)[:-3] + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    extra = os.environ.get("SQV_NVCC_EXTRA", "").split()  # dev A/B knobs (-D...)
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")

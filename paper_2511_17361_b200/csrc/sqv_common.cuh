@@ -38,14 +38,16 @@ constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
 // (sigma travels with the class weights, see prep's lrows.)
 constexpr int kRecWords = 40;
 struct __align__(16) PrimRec {
+  // words 0..32: everything the per-pair loop reads
   float2 HL[9];
   float2 G[3];
   float a, b, c;
-  float mcut;
   float cx, cy, cz;
+  float Ez[3];
+  // words 33..39: cull bound and window (block tests, partial blocks)
+  float mcut;
   int lo[3];
   int hi[3];
-  float Ez[3];
 };
 static_assert(sizeof(PrimRec) == kRecWords * 4, "PrimRec layout");
 

@@ -59,6 +59,31 @@ __device__ __forceinline__ float2 log2_1p_poly2(float2 t) {
   return fma2(t, bc2(1.442689896e+00f), mul2(t2, q));
 }
 
+// 2^x for x in [-125, 0] on the FMA pipe, packed: n = rint(x) by the
+// 1.5*2^23 shifter, f = x - n in [-0.5, 0.5] exactly, degree-6 minimax for
+// 2^f (max relative error 1.0e-7 evaluated in FP32, below MUFU.EX2's), the
+// exponent added as an integer.  x < -125 is clamped (callers only feed
+// arguments that are zeroed or < 2^-125 anyway).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x = make_float2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
+  const float2 j = add2(x, bc2(12582912.0f));
+  const float2 n = add2(j, bc2(-12582912.0f));
+  const float2 f = fma2(n, bc2(-1.0f), x);
+  float2 p = bc2(1.5345809515565634e-04f);
+  p = fma2(p, f, bc2(1.3399932067841291e-03f));
+  p = fma2(p, f, bc2(9.618489071726799e-03f));
+  p = fma2(p, f, bc2(5.550328642129898e-02f));
+  p = fma2(p, f, bc2(2.4022646248340607e-01f));
+  p = fma2(p, f, bc2(6.931471824645996e-01f));
+  p = fma2(p, f, bc2(1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
+#ifndef SQV_EXP_POLY
+#define SQV_EXP_POLY 0
+#endif
+
 // log2_acc on a pair: the exponent split is integer work per lane, the
 // polynomial runs packed.
 __device__ __forceinline__ float2 log2_acc2(float2 x) {
@@ -192,10 +217,15 @@ __device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords2&
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
+    // umin - umax = -|ux - uy| (the same rounded value); both coordinates 0
+    // give NaN, clamped to -126 (t ~ 0) while umax = -inf makes S^b = 0
     um[h] = make_float2(fmaxf(ux[h].x, uy[h].x), fmaxf(ux[h].y, uy[h].y));
-    const float2 mn = make_float2(fminf(ux[h].x, uy[h].x), fminf(ux[h].y, uy[h].y));
-    const float2 d = add2(mn, make_float2(-um[h].x, -um[h].y));
-    t[h] = make_float2(ex2(fmaxf(d.x, -126.0f)), ex2(fmaxf(d.y, -126.0f)));
+    const float2 dd = add2(ux[h], make_float2(-uy[h].x, -uy[h].y));
+    const float2 d = make_float2(fmaxf(-fabsf(dd.x), -126.0f), fmaxf(-fabsf(dd.y), -126.0f));
+    if (SQV_EXP_POLY >= 2)
+      t[h] = ex2_poly2(d);
+    else
+      t[h] = make_float2(ex2(d.x), ex2(d.y));
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) t[h] = log2_1p_poly2(t[h]);
@@ -204,12 +234,23 @@ __device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords2&
     const float2 e = mul2(bc2(b), add2(um[h], t[h]));
     F[h] = add2(make_float2(ex2(e.x), ex2(e.y)), make_float2(ex2(uz[h].x), ex2(uz[h].y)));
   }
+  // w = exp(-F) = 0 exactly once -F log2(e) < -126 (ftz), i.e. for every
+  // F > kFCut — the same zero the block cull assumes — so only the window
+  // test remains a select.  (F is never NaN: see above.)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float2 arg = mul2(F[h], bc2(-kLog2e));
-    const float e0 = ex2(arg.x), e1 = ex2(arg.y);
-    w[2 * h] = (cd.live[2 * h] & (F[h].x < kFCut)) ? e0 : 0.0f;
-    w[2 * h + 1] = (cd.live[2 * h + 1] & (F[h].y < kFCut)) ? e1 : 0.0f;
+    float e0, e1;
+    if (SQV_EXP_POLY >= 1) {
+      const float2 e = ex2_poly2(arg);
+      e0 = F[h].x < kFCut ? e.x : 0.0f;
+      e1 = F[h].y < kFCut ? e.y : 0.0f;
+    } else {
+      e0 = ex2(arg.x);
+      e1 = ex2(arg.y);
+    }
+    w[2 * h] = cd.live[2 * h] ? e0 : 0.0f;
+    w[2 * h + 1] = cd.live[2 * h + 1] ? e1 : 0.0f;
   }
 }
 
