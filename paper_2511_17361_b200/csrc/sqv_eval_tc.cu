@@ -47,16 +47,19 @@ template <int CM>
 struct TcShape {
   static_assert(CM + 1 <= kN, "sigma column must fit in N");
   static constexpr int kLRow = (CM + 1 + 3) & ~3;
-  static constexpr int kChunk = CM <= 18 ? 128 : 104;
+  static constexpr int kChunk = CM <= 18 ? 120 : 104;
   // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
   static constexpr int kA = 0;
   static constexpr int kB = kA + kWarps * 2 * 4096;
+  // staged primitives: record (40 words) + class weights/sigma (kLRow) each
+  static constexpr int kStride = kRecWords + kLRow;  // words
   static constexpr int kRec = kB + kWarps * 2 * 1024;
-  static constexpr int kLw = kRec + kChunk * kRecWords * 4;
-  // per-warp hit lists (chunk-local primitive indices, u8): primitives whose
-  // window covers the warp's whole block from the front, the rest from the back
-  static constexpr int kList = kLw + kChunk * kLRow * 4;
-  static constexpr int kBar = (kList + kWarps * kChunk + 7) & ~7;
+  // per-warp hit lists (offsets of staged primitives in 16 B units): primitives
+  // whose window covers the warp's whole block from the front, the rest from
+  // the back
+  static constexpr int kList = kRec + kChunk * kStride * 4;
+  static_assert(kStride % 4 == 0, "16-byte aligned staging");
+  static constexpr int kBar = (kList + kWarps * kChunk * 2 + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
   static constexpr int kEnd = kMisc + 4 + kWarps * 4;
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
@@ -77,9 +80,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   using S = TcShape<CM>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  float* s_rec = reinterpret_cast<float*>(smem + S::kRec);
-  float* s_lw = reinterpret_cast<float*>(smem + S::kLw);
-  uint8_t* s_list = smem + S::kList;
+  uint8_t* s_rec = smem + S::kRec;
+  uint16_t* s_list = reinterpret_cast<uint16_t*>(smem + S::kList);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
@@ -181,52 +183,63 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   for (int c0 = beg; c0 < end; c0 += S::kChunk) {
     const int n = min(S::kChunk, end - c0);
     __syncthreads();
-    for (int idx = tid; idx < n * (kRecWords / 4); idx += kThreads) {
-      const int j = idx / (kRecWords / 4), q = idx - j * (kRecWords / 4);
+    for (int idx = tid; idx < n * (S::kStride / 4); idx += kThreads) {
+      const int j = idx / (S::kStride / 4), q = idx - j * (S::kStride / 4);
       const int64_t g = fbase + A.prim_ids[c0 + j];
       reinterpret_cast<float4*>(s_rec)[idx] =
-          __ldg(reinterpret_cast<const float4*>(A.recs + g * kRecWords) + q);
-    }
-    for (int idx = tid; idx < n * (S::kLRow / 4); idx += kThreads) {
-      const int j = idx / (S::kLRow / 4), q = idx - j * (S::kLRow / 4);
-      const int64_t g = fbase + A.prim_ids[c0 + j];
-      reinterpret_cast<float4*>(s_lw)[idx] =
-          __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + q);
+          q < kRecWords / 4
+              ? __ldg(reinterpret_cast<const float4*>(A.recs + g * kRecWords) + q)
+              : __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + (q - kRecWords / 4));
     }
     __syncthreads();
-    uint8_t* lst = s_list + warp * S::kChunk;
+    uint16_t* lst = s_list + warp * S::kChunk;
     int n_in = 0, n_part = 0;  // warp-uniform list lengths
     const unsigned lt = (1u << lane) - 1u;
     for (int q = 0; q * 32 < n; ++q) {
       const int j = q * 32 + lane;
       bool hit = false, inside = false;
       if (j < n) {
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * S::kStride * 4);
         hit = block_may_hit(R, bx0, by0, bz0);
         inside = hit && block_inside(R, bx0, by0, bz0);
       }
       const unsigned mi = __ballot_sync(0xffffffffu, inside);
       const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
-      if (inside) lst[n_in + __popc(mi & lt)] = (uint8_t)j;
-      if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = (uint8_t)j;
+      const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
+      if (inside) lst[n_in + __popc(mi & lt)] = off;
+      if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = off;
       n_in += __popc(mi);
       n_part += __popc(mp);
     }
     __syncwarp();
-    auto visit = [&](int j, auto live) {
-      const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+    auto visit = [&](int off16, auto live) {
+      const int off = off16 << 4;
+      const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
       float w[kVPT];
       pair_weights<FIELD, decltype(live)::value>(R, x, y, z0, w);
       // class weight n = lane (sigma at CM), zero beyond
-      const float cw = lane < S::kLRow ? s_lw[j * S::kLRow + lane] : 0.0f;
+      const float cw =
+          lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane] : 0.0f;
       if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
       store_k(kk, w, cw);
       if (++kk == kK) issue();
     };
     // whole-block primitives first (no per-voxel window test), then the rest,
     // each in ascending primitive order
-    for (int i = 0; i < n_in; ++i) visit(lst[i], std::false_type{});
-    for (int i = 0; i < n_part; ++i) visit(lst[S::kChunk - 1 - i], std::true_type{});
+    // (the next offset is read one visit ahead; reads past a list end stay
+    // inside the CTA's shared memory and are discarded)
+    int off = lst[0];
+    for (int i = 0; i < n_in; ++i) {
+      const int next = lst[i + 1];
+      visit(off, std::false_type{});
+      off = next;
+    }
+    off = lst[S::kChunk - 1];
+    for (int i = 0; i < n_part; ++i) {
+      const int next = lst[S::kChunk - 2 - i];
+      visit(off, std::true_type{});
+      off = next;
+    }
   }
   if (kk > 0) {  // close the last K step with zero columns
     const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};

@@ -196,9 +196,12 @@ __device__ __forceinline__ float field_of(float x0, float x1, float x2, float a,
 
 // Strict mode (FIELD 6) takes the accurate logs for primitives whose exponent
 // amplifies the log error: 2/eps1 = c > 3.
+#ifndef SQV_ACC_C
+#define SQV_ACC_C 4.0f
+#endif
 template <int FIELD>
 __device__ __forceinline__ bool wants_acc(const PrimRec& R) {
-  return FIELD == 6 && R.c > 3.0f;
+  return FIELD == 6 && R.c > SQV_ACC_C;
 }
 
 // The log-sum-exp field of the column's 4 voxels as two packed voxel pairs:
