@@ -212,33 +212,93 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
       n_part += __popc(mp);
     }
     __syncwarp();
-    auto visit = [&](int off16, auto live) {
-      const int off = off16 << 4;
-      const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-      float w[kVPT];
-      pair_weights<FIELD, decltype(live)::value>(R, x, y, z0, w);
-      // class weight n = lane (sigma at CM), zero beyond
-      const float cw =
-          lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane] : 0.0f;
+    auto push = [&](const float(&w)[kVPT], float cw) {
       if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
       store_k(kk, w, cw);
       if (++kk == kK) issue();
     };
+    // class weight n = lane (sigma at CM), zero beyond
+    auto class_weight = [&](int off) {
+      return lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane]
+                             : 0.0f;
+    };
     // whole-block primitives first (no per-voxel window test), then the rest,
     // each in ascending primitive order
-    // (the next offset is read one visit ahead; reads past a list end stay
-    // inside the CTA's shared memory and are discarded)
-    int off = lst[0];
-    for (int i = 0; i < n_in; ++i) {
-      const int next = lst[i + 1];
-      visit(off, std::false_type{});
-      off = next;
-    }
-    off = lst[S::kChunk - 1];
-    for (int i = 0; i < n_part; ++i) {
-      const int next = lst[S::kChunk - 2 - i];
-      visit(off, std::true_type{});
-      off = next;
+    const int n_tot = n_in + n_part;
+    auto off_at = [&](int k) {
+      return (int)(k < n_in ? lst[k] : lst[S::kChunk - 1 - (k - n_in)]) << 4;
+    };
+    if constexpr (FIELD == 6 || FIELD == 7) {
+      // two-stage software pipeline: the logs of primitive k interleave with
+      // the exps of primitive k-1 (independent chains for the latency-bound
+      // SFU/FMA mix); the hand-off lives in registers
+      auto step = [&](int k, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
+        const int off = off_at(k);
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+        nxt.cw = class_weight(off);
+        const bool part = k >= n_in;
+        if (wants_acc<FIELD>(R)) {
+          if (part) {
+            stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
+            stage_exps<1>(cur, w);
+          } else {
+            stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
+            stage_exps<2>(cur, w);
+          }
+        } else {
+          if (part) {
+            stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
+            stage_exps<3>(cur, w);
+          } else {
+            stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
+            stage_exps<4>(cur, w);
+          }
+        }
+      };
+      if (n_tot > 0) {
+        PairState s0, s1;
+        float w[kVPT];
+        {
+          const int off = off_at(0);
+          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+          s0.cw = class_weight(off);
+          if (wants_acc<FIELD>(R)) {
+            if (n_in == 0)
+              stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
+            else
+              stage_logs<FIELD == 6, false, true>(R, x, y, z0, s0);
+          } else {
+            if (n_in == 0)
+              stage_logs<FIELD == 6, true, false>(R, x, y, z0, s0);
+            else
+              stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
+          }
+        }
+        int k = 1;
+        for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
+          step(k, s1, s0, w);
+          push(w, s0.cw);
+          step(k + 1, s0, s1, w);
+          push(w, s1.cw);
+        }
+        if (k < n_tot) {
+          step(k, s1, s0, w);
+          push(w, s0.cw);
+          stage_exps(s1, w);
+          push(w, s1.cw);
+        } else {
+          stage_exps(s0, w);
+          push(w, s0.cw);
+        }
+      }
+    } else {
+      for (int k = 0; k < n_tot; ++k) {
+        const int off = off_at(k);
+        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+        float w[kVPT];
+        pair_weights<FIELD, true>(R, x, y, z0, w);
+        push(w, class_weight(off));
+      }
     }
   }
   if (kk > 0) {  // close the last K step with zero columns

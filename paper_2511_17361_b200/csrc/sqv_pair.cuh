@@ -206,64 +206,73 @@ __device__ __forceinline__ bool wants_acc(const PrimRec& R) {
 
 // The log-sum-exp field of the column's 4 voxels as two packed voxel pairs:
 // the FMA-pipe work (scalings, the log2(1+t) polynomial, sums) issues once
-// per pair, the SFU work per voxel; the independent chains interleave.
-template <bool ACC>
-__device__ __forceinline__ void weights_lse4(const PrimRec& R, const ColCoords2& cd,
-                                             float (&w)[kVPT]) {
-  const float a = R.a, b = R.b, c = R.c;
-  float2 ux[2], uy[2], uz[2], um[2], t[2], F[2];
+// per pair, the SFU work per voxel.  Split in two stages so the evaluator can
+// software-pipeline primitives (stage_logs of the next primitive interleaves
+// with stage_exps of the current one); PairState is the hand-off.
+struct PairState {
+  float2 um[2], uz[2], t[2];
+  float b, cw;
+};
+
+// Stage 1: coordinates, the three logs, umax and t = 2^(umin - umax).  Dead
+// voxels (outside the window) get uz = +inf: Z = F = inf and w = 0.
+template <bool EXACT_STEP, bool LIVE, bool ACC>
+__device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z0,
+                                           PairState& S) {
+  ColCoords2 cd;
+  pair_coords<EXACT_STEP, LIVE>(R, x, y, z0, cd);
+  const float a = R.a, c = R.c;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    ux[h] = mul2(bc2(a), log2p<ACC>(cd.P[0][h]));
-    uy[h] = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
-    uz[h] = mul2(bc2(c), log2p<ACC>(cd.P[2][h]));
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
+    const float2 ux = mul2(bc2(a), log2p<ACC>(cd.P[0][h]));
+    const float2 uy = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
+    float2 uz = mul2(bc2(c), log2p<ACC>(cd.P[2][h]));
     // umin - umax = -|ux - uy| (the same rounded value); both coordinates 0
     // give NaN, clamped to -126 (t ~ 0) while umax = -inf makes S^b = 0
-    um[h] = make_float2(fmaxf(ux[h].x, uy[h].x), fmaxf(ux[h].y, uy[h].y));
-    const float2 dd = add2(ux[h], make_float2(-uy[h].x, -uy[h].y));
+    S.um[h] = make_float2(fmaxf(ux.x, uy.x), fmaxf(ux.y, uy.y));
+    const float2 dd = add2(ux, make_float2(-uy.x, -uy.y));
     const float2 d = make_float2(fmaxf(-fabsf(dd.x), -126.0f), fmaxf(-fabsf(dd.y), -126.0f));
     if (SQV_EXP_POLY >= 2)
-      t[h] = ex2_poly2(d);
+      S.t[h] = ex2_poly2(d);
     else
-      t[h] = make_float2(ex2(d.x), ex2(d.y));
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) t[h] = log2_1p_poly2(t[h]);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const float2 e = mul2(bc2(b), add2(um[h], t[h]));
-    F[h] = add2(make_float2(ex2(e.x), ex2(e.y)), make_float2(ex2(uz[h].x), ex2(uz[h].y)));
-  }
-  // w = exp(-F) = 0 exactly once -F log2(e) < -126 (ftz), i.e. for every
-  // F > kFCut — the same zero the block cull assumes — so only the window
-  // test remains a select.  (F is never NaN: see above.)
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const float2 arg = mul2(F[h], bc2(-kLog2e));
-    float e0, e1;
-    if (SQV_EXP_POLY >= 1) {
-      const float2 e = ex2_poly2(arg);
-      e0 = F[h].x < kFCut ? e.x : 0.0f;
-      e1 = F[h].y < kFCut ? e.y : 0.0f;
-    } else {
-      e0 = ex2(arg.x);
-      e1 = ex2(arg.y);
+      S.t[h] = make_float2(ex2(d.x), ex2(d.y));
+    if (LIVE) {
+      uz.x = cd.live[2 * h] ? uz.x : INFINITY;
+      uz.y = cd.live[2 * h + 1] ? uz.y : INFINITY;
     }
-    w[2 * h] = cd.live[2 * h] ? e0 : 0.0f;
-    w[2 * h + 1] = cd.live[2 * h + 1] ? e1 : 0.0f;
+    S.uz[h] = uz;
+  }
+  S.b = R.b;
+}
+
+// Stage 2: log2(1 + t), S^b, Z, F and w = exp(-F).  w = 0 exactly once
+// -F log2(e) < -126 (ftz), i.e. for every F > kFCut — the same zero the block
+// cull assumes — so no select is needed (F is never NaN: see above).
+// (TAG only keeps per-branch copies distinct, so the compiler cannot sink
+// them out of the branches that also hold the next primitive's stage_logs.)
+template <int TAG = 0>
+__device__ __forceinline__ void stage_exps(const PairState& S, float (&w)[kVPT]) {
+  if (TAG) asm volatile("// stage_exps %0" ::"n"(TAG));
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float2 l1p = log2_1p_poly2(S.t[h]);
+    const float2 e = mul2(bc2(S.b), add2(S.um[h], l1p));
+    const float2 F = add2(make_float2(ex2(e.x), ex2(e.y)), make_float2(ex2(S.uz[h].x), ex2(S.uz[h].y)));
+    const float2 arg = mul2(F, bc2(-kLog2e));
+    if (SQV_EXP_POLY >= 1) {
+      const float2 v = ex2_poly2(arg);
+      w[2 * h] = F.x < kFCut ? v.x : 0.0f;
+      w[2 * h + 1] = F.y < kFCut ? v.y : 0.0f;
+    } else {
+      w[2 * h] = ex2(arg.x);
+      w[2 * h + 1] = ex2(arg.y);
+    }
   }
 }
 
 template <int FIELD, bool ACC>
 __device__ __forceinline__ void weights_one(const PrimRec& R, const ColCoords2& cd,
                                             float (&w)[kVPT]) {
-  if (FIELD == 6 || FIELD == 7) {
-    weights_lse4<ACC>(R, cd, w);
-    return;
-  }
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) {
     const float x0 = (v & 1) ? cd.P[0][v >> 1].y : cd.P[0][v >> 1].x;
@@ -288,8 +297,17 @@ __device__ __forceinline__ void pair_field(const PrimRec& R, const ColCoords2& c
 template <int FIELD, bool LIVE = true>
 __device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int z0,
                                              float (&w)[kVPT]) {
+  if (FIELD == 6 || FIELD == 7) {
+    PairState S;
+    if (wants_acc<FIELD>(R))
+      stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, S);
+    else
+      stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, S);
+    stage_exps(S, w);
+    return;
+  }
   ColCoords2 cd;
-  pair_coords<FIELD == 6, LIVE>(R, x, y, z0, cd);
+  pair_coords<false, LIVE>(R, x, y, z0, cd);
   pair_field<FIELD>(R, cd, w);
 }
 
