@@ -183,13 +183,19 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   for (int c0 = beg; c0 < end; c0 += S::kChunk) {
     const int n = min(S::kChunk, end - c0);
     __syncthreads();
-    for (int idx = tid; idx < n * (S::kStride / 4); idx += kThreads) {
-      const int j = idx / (S::kStride / 4), q = idx - j * (S::kStride / 4);
-      const int64_t g = fbase + A.prim_ids[c0 + j];
-      reinterpret_cast<float4*>(s_rec)[idx] =
-          q < kRecWords / 4
-              ? __ldg(reinterpret_cast<const float4*>(A.recs + g * kRecWords) + q)
-              : __ldg(reinterpret_cast<const float4*>(A.lrows + g * A.lrow) + (q - kRecWords / 4));
+    {  // two threads per primitive, every 16-byte piece in flight at once
+      static_assert(2 * S::kChunk <= kThreads, "staging map");
+      const int j = tid >> 1;
+      if (j < n) {
+        const int64_t g = fbase + A.prim_ids[c0 + j];
+        const float4* rsrc = reinterpret_cast<const float4*>(A.recs + g * kRecWords);
+        const float4* lsrc = reinterpret_cast<const float4*>(A.lrows + g * A.lrow);
+        const uint32_t dst = tc::smem_u32(s_rec + j * S::kStride * 4);
+#pragma unroll
+        for (int q = tid & 1; q < S::kStride / 4; q += 2)
+          tc::cp_async16(dst + q * 16, q < kRecWords / 4 ? rsrc + q : lsrc + (q - kRecWords / 4));
+      }
+      tc::cp_async_wait_all();
     }
     __syncthreads();
     uint16_t* lst = s_list + warp * S::kChunk;
@@ -232,8 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
       // two-stage software pipeline: the logs of primitive k interleave with
       // the exps of primitive k-1 (independent chains for the latency-bound
       // SFU/FMA mix); the hand-off lives in registers
-      auto step = [&](int k, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
-        const int off = off_at(k);
+      auto step = [&](int k, int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
         const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
         nxt.cw = class_weight(off);
         const bool part = k >= n_in;
@@ -274,15 +279,19 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
               stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
           }
         }
-        int k = 1;
+        // list entries are read one step ahead (past the end: harmless reads
+        // inside the CTA's shared memory, discarded)
+        int k = 1, off = off_at(1);
         for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
-          step(k, s1, s0, w);
+          const int off1 = off_at(k + 1);
+          step(k, off, s1, s0, w);
           push(w, s0.cw);
-          step(k + 1, s0, s1, w);
+          off = off_at(k + 2);
+          step(k + 1, off1, s0, s1, w);
           push(w, s1.cw);
         }
         if (k < n_tot) {
-          step(k, s1, s0, w);
+          step(k, off, s1, s0, w);
           push(w, s0.cw);
           stage_exps(s1, w);
           push(w, s1.cw);
