@@ -145,8 +145,10 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
                           (uint32_t)(((lane >> 1) & 3) << 5);
   const uint32_t b_lane = (uint32_t)((lane & 7) * 4) | (uint32_t)(((lane >> 3) & 3) << 5);
   auto store_k = [&](int k, const float(&w)[kVPT], float cw) {
-    const uint32_t kq = (uint32_t)(k & 3) * 160u, kh = (uint32_t)(k & 4);
-    const uint32_t ao = a_lane ^ (kq | (kh << 9));
+    // slot part: (k & 3) * 160 | (k >> 2) << 11 (A), << 9 (B), as sums
+    const uint32_t k160 = (uint32_t)k * 160u, k4 = (uint32_t)(k & 4);
+    const uint32_t ao = a_lane ^ (k160 + k4 * 352u);
+    const uint32_t bo = b_lane ^ (k160 - k4 * 32u);
     float4 h, l;
     h.x = tf32_hi(w[0]);
     h.y = tf32_hi(w[1]);
@@ -158,7 +160,6 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     l.w = w[3] - h.w;
     *reinterpret_cast<float4*>(a_hi + ao) = h;
     *reinterpret_cast<float4*>(a_lo + ao) = l;
-    const uint32_t bo = b_lane ^ (kq | (kh << 7));
     const float ch = tf32_hi(cw);
     *reinterpret_cast<float*>(b_hi + bo) = ch;
     *reinterpret_cast<float*>(b_lo + bo) = cw - ch;
