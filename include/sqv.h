@@ -175,6 +175,29 @@ int sqv_confusion(const uint8_t* pred, const uint8_t* gt, int64_t n_voxels, int3
 int sqv_density(const sqv_prims* prims, const double* points, const int32_t* pair_prim,
                 int64_t n_points, float* F, float* density, void* stream);
 
+/*
+ * ray_iou.  pred/gt: [n_frames][V] u8 label grids
+ * (x-fastest; labels >= n_classes are free), host-side thresholds[n_thr]
+ * (metres, 1..16), device origins/dirs [n_rays][3] FP64 (unit dirs).  Per
+ * (frame, ray): first occupied voxel of pred and of gt along origin + t*dir
+ * by a 3D DDA; hit distance = t at which the ray enters that voxel (0 if the
+ * origin lies in it).  counts[n_thr][3] int64 (TP, FP, FN) are ACCUMULATED:
+ * TP when both hit with equal classes and |d_pred - d_gt| <= thr; a pred hit
+ * without a matching gt hit is an FP, a gt hit without a matching pred hit an
+ * FN.  hits (nullable) receives per-ray [n_frames][n_rays] distances (-1 = no
+ * hit) and classes (-1 = no hit).  Zero rays -> SQV_ERR_ARG ("zero rays").
+ */
+typedef struct sqv_ray_hits {
+  double* d_pred;
+  int32_t* c_pred;
+  double* d_gt;
+  int32_t* c_gt;
+} sqv_ray_hits;
+int sqv_ray_iou(const uint8_t* pred, const uint8_t* gt, int32_t n_frames, const sqv_grid* grid,
+                int32_t n_classes, const double* origins, const double* dirs, int64_t n_rays,
+                const double* thresholds, int32_t n_thr, int64_t* counts, sqv_ray_hits* hits,
+                void* stream);
+
 /* ---- instrumentation (bench / profiling; not part of the reference API) ----
  * When enabled, sqv_voxelize records CUDA events around its device stages on
  * the caller's stream and accumulates their durations:

@@ -3,7 +3,7 @@
 The oracle is the parity checker and CPU baseline of the B200 voxelizer.  It
 restates the reference's per-point math (/root/reference/pkg/src/sqocc/
 core.py:30-35,55-65,143-173,237-282) and the SPEC voxelize glue
-(/root/reference/SPEC.md:345-373,385,494-512) in plain C / FP64; see the header
+(/root/reference/SPEC.md:345-373,385,494-523) in plain C / FP64; see the header
 of sqv_oracle.c for the line-by-line map.  It is pinned against golden vectors
 produced by the reference's own ``sqocc.core`` (tests/golden/make_golden.py).
 
@@ -54,6 +54,8 @@ def lib():
         L.sqvo_density.argtypes = [i32, i32, P, P, P, P, P, P, P, P, i64, P, P]
         L.sqvo_set_threads.argtypes = [i32]
         L.sqvo_set_threads.restype = None
+        L.sqvo_ray_iou.argtypes = [i32, P, P, P, P, f64, i32, i64, P, P, i32, P, P, P, P, P, P]
+        L.sqvo_ray_iou.restype = None
         _lib = L
     return _lib
 
@@ -211,3 +213,26 @@ def density(p: Prims, points, pair_prim):
     if rc:
         raise InvalidPrimitive(-1, rc)
     return Fv, dv
+
+
+def ray_iou(pred, gt, dims, origin, resolution, n_classes, origins, dirs, thresholds):
+    """ray_iou counts.  pred/gt: [F][V] (or [V]) u8 labels,
+    x-fastest; origins/dirs [R,3].  Returns (counts [T,3] int64 TP/FP/FN,
+    hits dict of per-ray d/class arrays [F,R], class -1 = no hit)."""
+    pred = np.ascontiguousarray(pred, np.uint8)
+    gt = np.ascontiguousarray(gt, np.uint8)
+    V = int(np.prod(dims))
+    F = pred.size // V
+    origins = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+    dirs = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+    thr = np.ascontiguousarray(thresholds, np.float64).ravel()
+    R = origins.shape[0]
+    counts = np.zeros((thr.size, 3), np.int64)
+    dp = np.zeros((F, R)); dg = np.zeros((F, R))
+    cp = np.zeros((F, R), np.int32); cg = np.zeros((F, R), np.int32)
+    d = np.ascontiguousarray(dims, np.int32)
+    o = np.ascontiguousarray(origin, np.float64)
+    lib().sqvo_ray_iou(F, _p(pred), _p(gt), _p(d), _p(o), float(resolution),
+                       int(n_classes), R, _p(origins), _p(dirs), int(thr.size),
+                       _p(thr), _p(counts), _p(dp), _p(cp), _p(dg), _p(cg))
+    return counts, {"d_pred": dp, "c_pred": cp, "d_gt": dg, "c_gt": cg}

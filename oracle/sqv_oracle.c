@@ -18,6 +18,7 @@
  *   - finalize (tau, argmax lowest index) ........ SPEC.md:365-373
  *   - bins (tile -> ascending primitive ids) ..... SPEC.md:385 (tile shape pinned in include/sqv.h)
  *   - confusion counts for IoU / mIoU ............ SPEC.md:494-512,532
+ *   - ray_iou: DDA first hits, TP/FP/FN per threshold
  *
  * Parity pin: tests/golden/make_golden.py evaluates the reference's own
  * sqocc.core functions (imported from /root/reference) on seeded inputs and
@@ -445,4 +446,105 @@ int sqvo_density(int N, int C, const double* mu, const double* scale, const doub
     }
   free(P);
   return any_bad;
+}
+
+/* ---- ray_iou ----------------------------------------
+ * First occupied voxel (label < C) of a label grid [nz][ny][nx] (x-fastest,
+ * SPEC.md:392) along O + t*D, t >= 0, by a 3D DDA (Amanatides-Woo): slab
+ * entry into the grid box, start voxel by floor, then step the axis whose
+ * next boundary is nearest (ties: lowest axis).  Boundary times are
+ * recomputed from the lattice each step (no accumulated increments).  The
+ * hit distance is the t at which the ray enters the voxel (0 when the origin
+ * lies inside it).  FP64, no contraction: the device kernel evaluates the
+ * same expressions in the same order. */
+static int ray_first_hit(const uint8_t* lab, const int32_t* dims, const double* org, double res,
+                         int C, const double* O, const double* D, double* d_out, int* c_out) {
+  double t0 = 0.0, t1 = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    const double lo = org[a], hi = org[a] + (double)dims[a] * res;
+    if (D[a] == 0.0) {
+      if (!(O[a] >= lo && O[a] < hi)) return 0;
+    } else {
+      double ta = (lo - O[a]) / D[a], tb = (hi - O[a]) / D[a];
+      if (ta > tb) {
+        const double s = ta;
+        ta = tb;
+        tb = s;
+      }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+    }
+  }
+  if (!(t0 < t1)) return 0;
+  int i[3], step[3];
+  double tmax[3];
+  for (int a = 0; a < 3; ++a) {
+    const double p = O[a] + t0 * D[a];
+    double f = floor((p - org[a]) / res);
+    if (f < 0.0) f = 0.0;
+    if (f > (double)(dims[a] - 1)) f = (double)(dims[a] - 1);
+    i[a] = (int)f;
+    step[a] = D[a] > 0.0 ? 1 : (D[a] < 0.0 ? -1 : 0);
+    tmax[a] = step[a] == 0 ? INFINITY
+                           : (org[a] + (double)(i[a] + (step[a] > 0)) * res - O[a]) / D[a];
+  }
+  double t = t0;
+  for (;;) {
+    const uint8_t l = lab[i[0] + (int64_t)dims[0] * (i[1] + (int64_t)dims[1] * i[2])];
+    if (l < C) {
+      *d_out = t;
+      *c_out = l;
+      return 1;
+    }
+    int a = 0;
+    if (tmax[1] < tmax[a]) a = 1;
+    if (tmax[2] < tmax[a]) a = 2;
+    if (!(tmax[a] < t1)) return 0;
+    t = tmax[a];
+    i[a] += step[a];
+    if (i[a] < 0 || i[a] >= dims[a]) return 0;
+    tmax[a] = (org[a] + (double)(i[a] + (step[a] > 0)) * res - O[a]) / D[a];
+  }
+}
+
+/* Per-ray hits of pred and gt for F frames x R rays (frame-major outputs,
+ * class -1 = no hit) and the matching counts of SPEC.md:519-521 per
+ * threshold: counts[k][0..2] += TP, FP, FN.  A ray with both hits that fail
+ * to match (class or |d_pred - d_gt| > thr) is one FP and one FN. */
+void sqvo_ray_iou(int F, const uint8_t* pred, const uint8_t* gt, const int32_t* dims,
+                  const double* org, double res, int C, int64_t R, const double* origins,
+                  const double* dirs, int n_thr, const double* thr, int64_t* counts,
+                  double* d_pred, int32_t* c_pred, double* d_gt, int32_t* c_gt) {
+  const int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
+  for (int f = 0; f < F; ++f)
+    for (int64_t r = 0; r < R; ++r) {
+      double dp = 0.0, dg = 0.0;
+      int cp = -1, cg = -1;
+      const int hp = ray_first_hit(pred + f * V, dims, org, res, C, origins + 3 * r, dirs + 3 * r,
+                                   &dp, &cp);
+      const int hg = ray_first_hit(gt + f * V, dims, org, res, C, origins + 3 * r, dirs + 3 * r,
+                                   &dg, &cg);
+      const int64_t k = (int64_t)f * R + r;
+      if (d_pred) {
+        d_pred[k] = hp ? dp : -1.0;
+        c_pred[k] = hp ? cp : -1;
+        d_gt[k] = hg ? dg : -1.0;
+        c_gt[k] = hg ? cg : -1;
+      }
+      for (int j = 0; j < n_thr; ++j) {
+        int64_t* c = counts + 3 * j;
+        if (hp && hg) {
+          if (cp == cg && fabs(dp - dg) <= thr[j])
+            c[0]++;
+          else {
+            c[1]++;
+            c[2]++;
+          }
+        } else if (hp) {
+          c[1]++;
+        } else if (hg) {
+          c[2]++;
+        }
+      }
+    }
 }

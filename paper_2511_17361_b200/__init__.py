@@ -7,9 +7,11 @@ from .core import (EPS_MAX, EPS_MIN, F_CAP, ClassTable, PrimitiveBatch, Scene, S
                    quat_to_matrix)
 from .voxelize import (DenseGrids, SemanticGrid, VoxelGridSpec, VoxelizeConfig, VoxelizeResult,
                        Voxelizer, finalize, voxelize, voxelize_bruteforce)
+from .metrics import miou, ray_iou, voxel_iou
 
 __all__ = [
     "EPS_MIN", "EPS_MAX", "F_CAP", "SuperQuadric", "ClassTable", "Scene", "PrimitiveBatch",
     "quat_to_matrix", "VoxelGridSpec", "VoxelizeConfig", "DenseGrids", "SemanticGrid",
     "VoxelizeResult", "Voxelizer", "voxelize", "voxelize_bruteforce", "finalize",
+    "voxel_iou", "miou", "ray_iou",
 ]

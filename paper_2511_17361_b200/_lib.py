@@ -57,6 +57,10 @@ class SqvError(RuntimeError):
         self.code = code
 
 
+class RayHits(ctypes.Structure):
+    _fields_ = [("d_pred", _c_p), ("c_pred", _c_p), ("d_gt", _c_p), ("c_gt", _c_p)]
+
+
 _lib = None
 
 
@@ -87,8 +91,10 @@ def lib():
     L.sqv_profile_enable.argtypes = [ctypes.c_int]
     L.sqv_profile_read.argtypes = [_c_p, ctypes.POINTER(_i64), ctypes.c_int]
     L.sqv_microbench.argtypes = [ctypes.c_int, ctypes.POINTER(_f64), _c_p]
+    L.sqv_ray_iou.argtypes = [_c_p, _c_p, _i32, ctypes.POINTER(Grid), _i32, _c_p, _c_p, _i64,
+                              _c_p, _i32, _c_p, ctypes.POINTER(RayHits), _c_p]
     for f in ("sqv_voxelize", "sqv_finalize", "sqv_confusion", "sqv_density",
-              "sqv_profile_enable", "sqv_profile_read", "sqv_microbench"):
+              "sqv_profile_enable", "sqv_profile_read", "sqv_microbench", "sqv_ray_iou"):
         getattr(L, f).restype = ctypes.c_int
     if L.sqv_abi_version() != 1:
         raise RuntimeError("libsqv ABI version mismatch")
@@ -98,7 +104,8 @@ def lib():
 
 EXPORTED = ("sqv_abi_version", "sqv_last_error", "sqv_launch_count", "sqv_tiles_per_frame",
             "sqv_workspace_bytes", "sqv_voxelize", "sqv_finalize", "sqv_confusion",
-            "sqv_density", "sqv_profile_enable", "sqv_profile_read", "sqv_microbench")
+            "sqv_density", "sqv_profile_enable", "sqv_profile_read", "sqv_microbench",
+            "sqv_ray_iou")
 
 
 def last_error() -> str:

@@ -397,6 +397,45 @@ int sqv_density(const sqv_prims* prims, const double* points, const int32_t* pai
   return density_launch(prims, points, pair_prim, n_points, F, density, (cudaStream_t)stream);
 }
 
+int sqv_ray_iou(const uint8_t* pred, const uint8_t* gt, int32_t n_frames, const sqv_grid* grid,
+                int32_t n_classes, const double* origins, const double* dirs, int64_t n_rays,
+                const double* thresholds, int32_t n_thr, int64_t* counts, sqv_ray_hits* hits,
+                void* stream) {
+  if (!grid || !pred || !gt || !origins || !dirs || !counts || n_frames < 0)
+    return set_error(SQV_ERR_ARG, "invalid ray_iou arguments");
+  if (n_rays < 1) return set_error(SQV_ERR_ARG, "zero rays");
+  if (n_thr < 1 || n_thr > kMaxRayThr) return set_error(SQV_ERR_ARG, "1..16 thresholds");
+  if (n_classes < 1 || n_classes > 255) return set_error(SQV_ERR_ARG, "n_classes must lie in [1, 255]");
+  const int rc = check_grid(grid);
+  if (rc) return rc;
+  RayArgs A{};
+  A.pred = pred;
+  A.gt = gt;
+  for (int a = 0; a < 3; ++a) {
+    A.dims[a] = grid->dims[a];
+    A.org[a] = grid->origin[a];
+  }
+  A.res = grid->resolution;
+  A.n_classes = n_classes;
+  A.n_frames = n_frames;
+  A.n_rays = n_rays;
+  A.origins = origins;
+  A.dirs = dirs;
+  A.n_thr = n_thr;
+  for (int j = 0; j < n_thr; ++j) {
+    if (!(thresholds[j] >= 0.0)) return set_error(SQV_ERR_ARG, "thresholds must be >= 0");
+    A.thr[j] = thresholds[j];
+  }
+  A.counts = reinterpret_cast<unsigned long long*>(counts);
+  if (hits) {
+    A.d_pred = hits->d_pred;
+    A.c_pred = hits->c_pred;
+    A.d_gt = hits->d_gt;
+    A.c_gt = hits->c_gt;
+  }
+  return ray_iou_launch(A, (cudaStream_t)stream);
+}
+
 int sqv_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   g_prof.on = on != 0;

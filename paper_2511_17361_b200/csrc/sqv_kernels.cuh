@@ -77,6 +77,29 @@ int finalize_launch(const float* v_o, const float* v_c, int64_t n, int C, float 
 int confusion_launch(const uint8_t* pred, const uint8_t* gt, int64_t n, int C, int64_t* cm,
                      cudaStream_t s);
 int microbench(int which, double* ops_per_s, cudaStream_t s);
+// ray_iou (sqv_ray.cu)
+constexpr int kMaxRayThr = 16;
+struct RayArgs {
+  const uint8_t* pred;
+  const uint8_t* gt;
+  int dims[3];
+  double org[3];
+  double res;
+  int n_classes;
+  int n_frames;
+  int64_t n_rays;
+  const double* origins;
+  const double* dirs;
+  int n_thr;
+  double thr[kMaxRayThr];
+  unsigned long long* counts;
+  double* d_pred;
+  int32_t* c_pred;
+  double* d_gt;
+  int32_t* c_gt;
+};
+int ray_iou_launch(const RayArgs& A, cudaStream_t s);
+
 int density_launch(const sqv_prims* P, const double* points, const int32_t* pair_prim,
                    int64_t n, float* F, float* density, cudaStream_t s);
 
