@@ -9,9 +9,10 @@ namespace sqv {
 constexpr int kVPT = 4;  // voxels per thread: a 1x1x4 z-column
 
 // Can primitive R contribute to the warp's 4x4x8 voxel block at (bx0, by0,
-// bz0)?  Window overlap, then a conservative geometric test: the block's
+// bz0)?  Window overlap, then conservative geometric tests: the block's
 // centre in local coordinates minus its local half extent must come within
-// mcut on every axis (else max|x'| > mcut on the whole block, F > kFCut).
+// mcut on every axis (else max|x'| > mcut on the whole block, F > kFCut),
+// and the field at the nearest corner of that local box must be below kFCut.
 // Evaluated lane-parallel (one primitive per lane) when building the masks.
 __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0, int bz0) {
   if (bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
@@ -19,17 +20,26 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
     return false;
   const float kx = (float)bx0 + 1.5f - R.cx, ky = (float)by0 + 1.5f - R.cy,
               kz = (float)bz0 + 3.5f - R.cz;
-  float dmax = -1.0f, slack = 0.0f;
+  float dmax = -1.0f, slack = 0.0f, m[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const float ex = R.HL[3 * r].x + R.HL[3 * r].y, ey = R.HL[3 * r + 1].x + R.HL[3 * r + 1].y,
                 ez = R.HL[3 * r + 2].x + R.HL[3 * r + 2].y;
     const float c = fmaf(kz, ez, fmaf(ky, ey, fmaf(kx, ex, R.G[r].x + R.G[r].y)));
     const float h = 1.5f * fabsf(ex) + 1.5f * fabsf(ey) + 3.5f * fabsf(ez);
-    dmax = fmaxf(dmax, fabsf(c) - h);
+    m[r] = fabsf(c) - h;
+    dmax = fmaxf(dmax, m[r]);
     slack += fabsf(c) + h;
   }
-  return dmax <= R.mcut + 1e-4f * slack;
+  const float e = 1e-4f * slack;  // covers the FP32 error of c and h
+  if (dmax > R.mcut + e) return false;
+  // Tighter: F grows with each |x'_r|, so over the block F >= F at the
+  // box corner nearest the centre, |x'_r| >= max(|c_r| - h_r, 0).  Culled
+  // only with a 2% margin over kFCut, far above the SFU field error, so every
+  // culled pair would have had F > kFCut, i.e. w = 0 exactly.
+  const float F = field_F(fmaxf(m[0] - e, 0.0f), fmaxf(m[1] - e, 0.0f), fmaxf(m[2] - e, 0.0f),
+                          R.a, R.b, R.c);
+  return F < 1.02f * kFCut;
 }
 
 // Is the warp's whole 4x4x8 block inside R's window?  Then no voxel of the
