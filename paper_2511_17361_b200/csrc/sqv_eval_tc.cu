@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     s_vo[vz * zpo + loc] = vo;
     s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
   }
+  tc::fence_proxy_async_smem();  // staging -> visible to the bulk-copy engine
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) {
@@ -376,30 +377,57 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   const int64_t V = (int64_t)nx * ny * nz;
   const int xw = min(kTileX, nx - x_t);
   const int yy = y_t + warp;
-  if (yy < ny) {
-    const int zend = min(kTileZ, nz - z_t);
-    int64_t gv = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
-    const int64_t zstep = (int64_t)nx * ny;
-    const int nel = xw * C;
-    const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
-    const int nel4 = nel >> 2;
-    for (int zl = 0; zl < zend; ++zl, gv += zstep) {
-      const int row = zl * kTileY + warp;
-      if (A.v_c) {
-        const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
-        float* dst = A.v_c + gv * C;
-        if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-          const float4* s4 = reinterpret_cast<const float4*>(src);
-          float4* d4 = reinterpret_cast<float4*>(dst);
-          for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
-        } else {
-          for (int e = lane; e < nel; e += 32) dst[e] = src[e];
-        }
+  if (yy >= ny) return;
+  const int zend = min(kTileZ, nz - z_t);
+  const int64_t gv0 = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
+  const int64_t zstep = (int64_t)nx * ny;
+  // Full rows whose global addresses are 16-byte aligned go out as bulk
+  // async copies (one lane per z layer: the v_c row of 8*C floats and the
+  // v_o row of 8 floats) and one 8-byte label store; the rest take the
+  // lane-parallel path.  Alignment is uniform per launch (row and layer
+  // strides), so the choice is warp-uniform.
+  const bool full = xw == kTileX;
+  const bool vc_bulk = !A.v_c || (full && ((nx * C) & 3) == 0 && ((V * C) & 3) == 0 &&
+                                  (reinterpret_cast<uintptr_t>(A.v_c) & 15) == 0);
+  const bool vo_bulk = !A.v_o || (full && (nx & 3) == 0 && (V & 3) == 0 &&
+                                  (reinterpret_cast<uintptr_t>(A.v_o) & 15) == 0);
+  const bool lab8 = full && (nx & 7) == 0 && (V & 7) == 0 &&
+                    (reinterpret_cast<uintptr_t>(A.labels) & 7) == 0;
+  if (vc_bulk && vo_bulk && lab8) {
+    if (lane < zend) {
+      const int zl = lane;
+      const int64_t gv = gv0 + zl * zstep;
+      if (A.v_c)
+        tc::bulk_store(A.v_c + gv * C, tc::smem_u32(s_vc + zl * zpc + warp * kTileX * C),
+                       (uint32_t)(kTileX * C * 4));
+      if (A.v_o)
+        tc::bulk_store(A.v_o + gv, tc::smem_u32(s_vo + zl * zpo + warp * kTileX),
+                       (uint32_t)(kTileX * 4));
+      *reinterpret_cast<uint2*>(A.labels + gv) =
+          *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
+      tc::bulk_commit_wait_read();  // staging must outlive the copies' reads
+    }
+    return;
+  }
+  int64_t gv = gv0;
+  const int nel = xw * C;
+  const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
+  const int nel4 = nel >> 2;
+  for (int zl = 0; zl < zend; ++zl, gv += zstep) {
+    if (A.v_c) {
+      const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
+      float* dst = A.v_c + gv * C;
+      if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
+      } else {
+        for (int e = lane; e < nel; e += 32) dst[e] = src[e];
       }
-      if (lane < xw) {
-        if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
-        A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
-      }
+    }
+    if (lane < xw) {
+      if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
+      A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
     }
   }
 }
