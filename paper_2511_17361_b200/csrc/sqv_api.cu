@@ -43,6 +43,30 @@ struct Header {  // device-side scalars, read back in one 32-byte copy
   long long pad;
 };
 
+// The one mid-pipeline readback goes through a mapped pinned buffer written
+// by a one-thread kernel: no copy engine is involved, so the readback never
+// queues behind a caller's bulk H2D/D2H traffic on other streams (the
+// overlapped stream API copies ~100 MB per batch).  One buffer per host
+// thread; calls on a thread are sequential (each waits for its readback).
+__global__ void header_out_kernel(const Header* src, Header* dst) {
+  volatile long long* d = reinterpret_cast<volatile long long*>(dst);
+  const long long* s = reinterpret_cast<const long long*>(src);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d[k] = s[k];
+}
+
+static Header* mapped_header() {
+  static thread_local Header* h = nullptr;
+  if (!h) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, sizeof(Header), cudaHostAllocMapped | cudaHostAllocPortable) !=
+        cudaSuccess)
+      return nullptr;
+    h = static_cast<Header*>(p);
+  }
+  return h;
+}
+
 struct Layout {
   size_t hdr, recs, lrows, counts, offs, windows, tile_cnt, tile_off, scan_tmp;  // fixed
   size_t keys_a, vals_a, keys_b, vals_b, radix_tmp;                              // variable
@@ -214,12 +238,13 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   float* recs = (float*)(ws + L.recs);
   float* lrows = (float*)(ws + L.lrows);
 
-  Header h0;
-  std::memset(&h0, 0, sizeof(h0));
-  h0.bad_word = ~0ULL;
-  if (cudaMemcpyAsync(hdr, &h0, sizeof(h0), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+  // header: zeros, bad_word = ~0 (memset kernels, no host copy)
+  if (cudaMemsetAsync(hdr, 0, sizeof(Header), s) != cudaSuccess ||
+      cudaMemsetAsync(&hdr->bad_word, 0xFF, sizeof(hdr->bad_word), s) != cudaSuccess ||
       cudaMemsetAsync(tile_cnt, 0, (size_t)(FT + 1) * 4, s) != cudaSuccess)
     return check_launch("workspace init");
+  Header* hmap = mapped_header();
+  if (!hmap) return set_error(SQV_ERR_CUDA, "mapped header allocation failed");
 
   const bool prof = g_prof.on;
   if (prof) {
@@ -257,10 +282,15 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   // K2 scan of per-primitive tile counts -> entry offsets, total -> header
   if (int rc = scan_exclusive(counts, offs, FN, scan_tmp, &hdr->n_entries, s)) return rc;
   if (prof) cudaEventRecord(g_prof.ev[1], s);
+  header_out_kernel<<<1, 1, 0, s>>>(hdr, hmap);
+  count_launch();
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("header readback");
   Header h;
-  if (cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return check_launch("header readback");
+  {
+    const volatile long long* m = reinterpret_cast<const volatile long long*>(hmap);
+    long long* d = reinterpret_cast<long long*>(&h);
+    for (int k = 0; k < 4; ++k) d[k] = m[k];
+  }
   if (prof) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.fold_pending();
