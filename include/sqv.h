@@ -198,6 +198,19 @@ int sqv_ray_iou(const uint8_t* pred, const uint8_t* gt, int32_t n_frames, const 
                 const double* thresholds, int32_t n_thr, int64_t* counts, sqv_ray_hits* hits,
                 void* stream);
 
+/*
+ * Device-side seeded scene generation (gen_scene): frames
+ * first_frame .. first_frame+n_frames-1 of the Philox4x32-10 stream `seed`,
+ * written as the FP64 SoA inputs of sqv_voxelize (device pointers, frame
+ * major): mu ~ U(grid bounds), scale ~ U[smin, smax], rot = normalised
+ * N(0,1)^4, opacity ~ U[0,1], eps ~ U[emin, 2], logits ~ N(0,1).  A frame's
+ * primitives depend only on (seed, frame index, primitive index).
+ */
+int sqv_gen_frames(uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t n_prims,
+                   int32_t n_classes, const sqv_grid* grid, double smin, double smax,
+                   double emin, double* mu, double* scale, double* rot, double* opacity,
+                   double* eps, double* logits, void* stream);
+
 /* ---- instrumentation (bench / profiling; not part of the reference API) ----
  * When enabled, sqv_voxelize records CUDA events around its device stages on
  * the caller's stream and accumulates their durations:

@@ -93,8 +93,11 @@ def lib():
     L.sqv_microbench.argtypes = [ctypes.c_int, ctypes.POINTER(_f64), _c_p]
     L.sqv_ray_iou.argtypes = [_c_p, _c_p, _i32, ctypes.POINTER(Grid), _i32, _c_p, _c_p, _i64,
                               _c_p, _i32, _c_p, ctypes.POINTER(RayHits), _c_p]
+    L.sqv_gen_frames.argtypes = [ctypes.c_uint64, _i64, _i32, _i32, _i32, ctypes.POINTER(Grid),
+                                 _f64, _f64, _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]
     for f in ("sqv_voxelize", "sqv_finalize", "sqv_confusion", "sqv_density",
-              "sqv_profile_enable", "sqv_profile_read", "sqv_microbench", "sqv_ray_iou"):
+              "sqv_profile_enable", "sqv_profile_read", "sqv_microbench", "sqv_ray_iou",
+              "sqv_gen_frames"):
         getattr(L, f).restype = ctypes.c_int
     if L.sqv_abi_version() != 1:
         raise RuntimeError("libsqv ABI version mismatch")
@@ -105,7 +108,7 @@ def lib():
 EXPORTED = ("sqv_abi_version", "sqv_last_error", "sqv_launch_count", "sqv_tiles_per_frame",
             "sqv_workspace_bytes", "sqv_voxelize", "sqv_finalize", "sqv_confusion",
             "sqv_density", "sqv_profile_enable", "sqv_profile_read", "sqv_microbench",
-            "sqv_ray_iou")
+            "sqv_ray_iou", "sqv_gen_frames")
 
 
 def last_error() -> str:

@@ -466,6 +466,41 @@ int sqv_ray_iou(const uint8_t* pred, const uint8_t* gt, int32_t n_frames, const 
   return ray_iou_launch(A, (cudaStream_t)stream);
 }
 
+int sqv_gen_frames(uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t n_prims,
+                   int32_t n_classes, const sqv_grid* grid, double smin, double smax,
+                   double emin, double* mu, double* scale, double* rot, double* opacity,
+                   double* eps, double* logits, void* stream) {
+  if (n_frames < 0 || n_prims < 0 || n_classes < 1 || first_frame < 0)
+    return set_error(SQV_ERR_ARG, "invalid gen_frames sizes");
+  if (!(smin > 0.0 && smax >= smin && std::isfinite(smax)))
+    return set_error(SQV_ERR_ARG, "scales must satisfy 0 < smin <= smax");
+  if (!(emin > 0.0 && emin <= 2.0)) return set_error(SQV_ERR_ARG, "emin must lie in (0, 2]");
+  const int rc = check_grid(grid);
+  if (rc) return rc;
+  if ((int64_t)n_frames * n_prims > 0 && (!mu || !scale || !rot || !opacity || !eps || !logits))
+    return set_error(SQV_ERR_ARG, "output arrays are NULL");
+  GenArgs A{};
+  A.seed = seed;
+  A.first_frame = first_frame;
+  A.n_frames = n_frames;
+  A.n_prims = n_prims;
+  A.n_classes = n_classes;
+  for (int a = 0; a < 3; ++a) {
+    A.lo[a] = grid->origin[a];
+    A.hi[a] = grid->origin[a] + (double)grid->dims[a] * grid->resolution;
+  }
+  A.smin = smin;
+  A.smax = smax;
+  A.emin = emin;
+  A.mu = mu;
+  A.scale = scale;
+  A.rot = rot;
+  A.opacity = opacity;
+  A.eps = eps;
+  A.logits = logits;
+  return gen_launch(A, (cudaStream_t)stream);
+}
+
 int sqv_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   g_prof.on = on != 0;

@@ -77,6 +77,17 @@ int finalize_launch(const float* v_o, const float* v_c, int64_t n, int C, float 
 int confusion_launch(const uint8_t* pred, const uint8_t* gt, int64_t n, int C, int64_t* cm,
                      cudaStream_t s);
 int microbench(int which, double* ops_per_s, cudaStream_t s);
+// device scene generation (sqv_gen.cu)
+struct GenArgs {
+  uint64_t seed;
+  int64_t first_frame;
+  int n_frames, n_prims, n_classes;
+  double lo[3], hi[3];
+  double smin, smax, emin;
+  double *mu, *scale, *rot, *opacity, *eps, *logits;
+};
+int gen_launch(const GenArgs& A, cudaStream_t s);
+
 // ray_iou (sqv_ray.cu)
 constexpr int kMaxRayThr = 16;
 struct RayArgs {

@@ -47,3 +47,48 @@ def evaluate_stream(voxelizer, batches, gt_labels, n_classes: int, group=None):
         r = voxelizer(batch, dense=False)
         confusion_matrix(r.labels, gt, n_classes, out=cm)
     return allreduce_confusion(cm, group)
+
+
+def evaluate_generated(voxelizer, seed: int, n_frames: int, n_prims: int,
+                       frames_per_batch: int = 100, gt_seed: int | None = None,
+                       sigma_mu: float = 0.2, sigma_logit: float = 0.5, smin: float = 0.2,
+                       smax: float = 4.0, emin: float = 0.2, group=None):
+    """The config-5 stream with no host in the loop: this rank's frame shard
+    is generated in HBM (``scenegen.gen_frames_device``: frame f depends only
+    on (seed, f), so shards need no coordination), the ground truth is a
+    jittered copy (mu + N(0, sigma_mu), logits + N(0, sigma_logit), device
+    RNG seeded per batch), both are voxelized and their confusion counts
+    accumulated, then all-reduced once.  Returns the global counts."""
+    import torch
+    import torch.distributed as dist
+    from .core import PrimitiveBatch
+    from .metrics import confusion_matrix
+    from .scenegen import gen_frames_device
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    C = voxelizer.C
+    spec = voxelizer.spec
+    dev = voxelizer.device
+    gt_seed = seed + 1 if gt_seed is None else gt_seed
+    K = C + 1
+    cm = torch.zeros((K, K), dtype=torch.int64, device=dev)
+    start, stop = shard_frames(n_frames, rank, world)
+    for f0 in range(start, stop, frames_per_batch):
+        F = min(frames_per_batch, stop - f0)
+        b = gen_frames_device(seed, F, n_prims, C, origin=spec.origin, dims=spec.dims,
+                              resolution=spec.resolution, smin=smin, smax=smax, emin=emin,
+                              first_frame=f0, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(int(gt_seed) * 1000003 + f0)
+        gt = PrimitiveBatch(b.mu + sigma_mu * torch.randn(b.mu.shape, generator=g, device=dev,
+                                                          dtype=torch.float64),
+                            b.scale, b.rot, b.opacity, b.eps,
+                            b.logits + sigma_logit * torch.randn(b.logits.shape, generator=g,
+                                                                 device=dev,
+                                                                 dtype=torch.float64))
+        pred_l = voxelizer(b, dense=False).labels
+        gt_l = voxelizer(gt, dense=False).labels
+        confusion_matrix(pred_l, gt_l, C, out=cm)
+    return allreduce_confusion(cm, group)

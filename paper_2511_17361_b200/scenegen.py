@@ -73,3 +73,35 @@ def jitter(batch: PrimitiveBatch, seed: int, sigma_mu: float = 0.2,
     return PrimitiveBatch(mu, np.asarray(batch.scale), np.asarray(batch.rot),
                           np.asarray(batch.opacity), np.asarray(batch.eps), logits,
                           n_valid=batch.n_valid)
+
+
+def gen_frames_device(seed: int, n_frames: int, n_prims: int, n_classes: int = 18,
+                      origin=(-40.0, -40.0, -1.0), dims=(200, 200, 16), resolution: float = 0.4,
+                      smin: float = 0.2, smax: float = 4.0, emin: float = 0.2,
+                      first_frame: int = 0, device=None, stream=None) -> PrimitiveBatch:
+    """The same distributions generated in HBM by the ``sqv_gen_frames``
+    kernel (Philox4x32-10 counter stream; include/sqv.h): a PrimitiveBatch of
+    device tensors, ready for ``Voxelizer``.  A different (counter-based)
+    stream than ``gen_frames``: frame f of (seed, first_frame) depends only on
+    seed and first_frame + f, so ranks generate their own shards."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .voxelize import VoxelGridSpec
+    dev = _lib.require_cuda() if device is None else torch.device(device)
+    L = _lib.lib()
+    if not (0 <= seed < 2 ** 64):
+        raise ValueError("seed must be a 64-bit unsigned integer")
+    F, N, C = int(n_frames), int(n_prims), int(n_classes)
+    mk = lambda *s: torch.empty((F, N) + s, dtype=torch.float64, device=dev)
+    mu, scale, rot, opacity, eps, logits = mk(3), mk(3), mk(4), mk(), mk(2), mk(C)
+    g = VoxelGridSpec(origin=tuple(origin), dims=tuple(dims), resolution=resolution)._c()
+    s = stream if stream is not None else _lib.stream_ptr(dev)
+    with torch.cuda.device(dev):
+        _lib.check(L.sqv_gen_frames(int(seed), int(first_frame), F, N, C, ctypes.byref(g),
+                                    float(smin), float(smax), float(emin), mu.data_ptr(),
+                                    scale.data_ptr(), rot.data_ptr(), opacity.data_ptr(),
+                                    eps.data_ptr(), logits.data_ptr(), s), "sqv_gen_frames")
+    return PrimitiveBatch(mu, scale, rot, opacity, eps, logits)
