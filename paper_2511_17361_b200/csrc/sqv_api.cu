@@ -40,7 +40,7 @@ struct Header {  // device-side scalars, read back in one 32-byte copy
   long long n_entries;
   unsigned long long bad_word;
   unsigned long long n_pairs;
-  long long pad;
+  long long pad;  // low word: the persistent evaluator's tile counter
 };
 
 // The one mid-pipeline readback goes through a mapped pinned buffer written
@@ -368,6 +368,9 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.labels = out->labels;
   A.v_o = out->v_o;
   A.v_c = out->v_c;
+  A.n_tiles = (int)FT;
+  A.tile_counter = reinterpret_cast<int*>(&hdr->pad);  // zeroed with the header
+  A.n_entries = E;
   if (prof) cudaEventRecord(g_prof.ev[3], s);
   {
     // tcgen05 evaluator by default; SQV_EVAL=ffma selects the CUDA-core one (A/B runs)

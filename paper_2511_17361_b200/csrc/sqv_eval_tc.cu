@@ -36,6 +36,7 @@ namespace sqv {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPersistentBelow = 64;  // mean primitives per tile
 constexpr int kWarps = 8;
 constexpr int kMaxChunk = 128;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
@@ -61,7 +62,7 @@ struct TcShape {
   static_assert(kStride % 4 == 0, "16-byte aligned staging");
   static constexpr int kBar = (kList + kWarps * kChunk * 2 + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
-  static constexpr int kEnd = kMisc + 4 + kWarps * 4;
+  static constexpr int kEnd = kMisc + 4 + kWarps * 4 + 4;  // + next-tile slot
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
   // holding z-adjacent voxels hit different banks
   static constexpr int kStage = 16 * ((64 * CM + 8) * 4 + 72 * 4 + 72);
@@ -75,7 +76,7 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-template <int CM, int FIELD>
+template <int CM, int FIELD, bool PERSIST>
 __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   using S = TcShape<CM>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -86,19 +87,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
 
-  const int tile_g = blockIdx.x;
-  const int f = tile_g / A.tiles_per_frame;
-  const int t = tile_g - f * A.tiles_per_frame;
-  const int tx = t % A.ntx;
-  const int ty = (t / A.ntx) % A.nty;
-  const int tz = t / (A.ntx * A.nty);
+  int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + kWarps * 4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bx0 = tx * kTileX + (warp & 1) * 4;
-  const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
-  const int bz0 = tz * kTileZ + (warp >> 2) * 8;
-  const int x = bx0 + (lane & 3);
-  const int y = by0 + ((lane >> 2) & 3);
-  const int z0 = bz0 + (lane >> 4) * 4;
 
   // ---- TMEM + barriers ----
   if (warp == 0) {
@@ -179,25 +169,53 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     pending = true;
     kk = 0;
   };
+  // ---- persistent loop over tiles: tile 0 of this CTA is blockIdx.x, the
+  // rest come from a global counter (dynamic balance; tiles vary from 0 to
+  // hundreds of primitives).  TMEM, barriers and descriptors are set up once;
+  // the first chunk of the next tile is staged (cp.async) while the epilogue
+  // of the current one runs when the epilogue staging leaves s_rec alone.
+  constexpr bool kPrefetch = S::kStage <= S::kRec;
+  auto stage_chunk = [&](int64_t fb, int c0, int n) {
+    // two threads per primitive, every 16-byte piece in flight at once
+    static_assert(2 * S::kChunk <= kThreads, "staging map");
+    const int j = tid >> 1;
+    if (j < n) {
+      const int64_t g = fb + A.prim_ids[c0 + j];
+      const float4* rsrc = reinterpret_cast<const float4*>(A.recs + g * kRecWords);
+      const float4* lsrc = reinterpret_cast<const float4*>(A.lrows + g * A.lrow);
+      const uint32_t dst = tc::smem_u32(s_rec + j * S::kStride * 4);
+#pragma unroll
+      for (int q = tid & 1; q < S::kStride / 4; q += 2)
+        tc::cp_async16(dst + q * 16, q < kRecWords / 4 ? rsrc + q : lsrc + (q - kRecWords / 4));
+    }
+  };
+  int tile_g = blockIdx.x;
+  bool prefetched = false;
+  while (tile_g < A.n_tiles) {
+  const int f = tile_g / A.tiles_per_frame;
+  const int t = tile_g - f * A.tiles_per_frame;
+  const int tx = t % A.ntx;
+  const int ty = (t / A.ntx) % A.nty;
+  const int tz = t / (A.ntx * A.nty);
+  const int bx0 = tx * kTileX + (warp & 1) * 4;
+  const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
+  const int bz0 = tz * kTileZ + (warp >> 2) * 8;
+  const int x = bx0 + (lane & 3);
+  const int y = by0 + ((lane >> 2) & 3);
+  const int z0 = bz0 + (lane >> 4) * 4;
+  kk = 0;
+  groups = 0;
+  // claim the next tile now; the result is only needed at the epilogue
+  const int claimed = (PERSIST && tid == 0) ? atomicAdd(A.tile_counter, 1) : 0;
   const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
   const int64_t fbase = (int64_t)f * A.n_prims;
   for (int c0 = beg; c0 < end; c0 += S::kChunk) {
     const int n = min(S::kChunk, end - c0);
-    __syncthreads();
-    {  // two threads per primitive, every 16-byte piece in flight at once
-      static_assert(2 * S::kChunk <= kThreads, "staging map");
-      const int j = tid >> 1;
-      if (j < n) {
-        const int64_t g = fbase + A.prim_ids[c0 + j];
-        const float4* rsrc = reinterpret_cast<const float4*>(A.recs + g * kRecWords);
-        const float4* lsrc = reinterpret_cast<const float4*>(A.lrows + g * A.lrow);
-        const uint32_t dst = tc::smem_u32(s_rec + j * S::kStride * 4);
-#pragma unroll
-        for (int q = tid & 1; q < S::kStride / 4; q += 2)
-          tc::cp_async16(dst + q * 16, q < kRecWords / 4 ? rsrc + q : lsrc + (q - kRecWords / 4));
-      }
-      tc::cp_async_wait_all();
+    if (!(prefetched && c0 == beg)) {
+      __syncthreads();  // every warp is done with the previous chunk
+      stage_chunk(fbase, c0, n);
     }
+    tc::cp_async_wait_all();
     __syncthreads();
     uint16_t* lst = s_list + warp * S::kChunk;
     int n_in = 0, n_part = 0;  // warp-uniform list lengths
@@ -318,9 +336,21 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   }
   wait_free();
   if (lane == 0) s_has[warp] = groups > 0;
+  // next tile (one atomic per CTA), published by the barrier below
+  if (PERSIST && tid == 0) *s_next = (int)gridDim.x + claimed;
   tc::fence_before_sync();
   __syncthreads();  // all MMAs complete; operand smem is free for staging
   tc::fence_after_sync();
+  const int next_tile = PERSIST ? *s_next : A.n_tiles;
+  prefetched = false;
+  if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
+    const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
+    if (ne > nb) {
+      const int nf = next_tile / A.tiles_per_frame;
+      stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
+      prefetched = true;
+    }
+  }
 
   // ---- epilogue: TMEM -> finalize -> staged coalesced stores -------------
   const int C = A.n_classes;
@@ -368,16 +398,13 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   tc::fence_proxy_async_smem();  // staging -> visible to the bulk-copy engine
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc(tmem_base, kTmemCols);
-  }
+  tc::fence_after_sync();
   // rows of 8 voxels: this warp owns y row y_t + warp (8 warps = the tile's
   // 8 y rows) for every z layer, so the row base just steps by nx*ny
   const int64_t V = (int64_t)nx * ny * nz;
   const int xw = min(kTileX, nx - x_t);
   const int yy = y_t + warp;
-  if (yy >= ny) return;
+  if (yy < ny) {
   const int zend = min(kTileZ, nz - z_t);
   const int64_t gv0 = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
   const int64_t zstep = (int64_t)nx * ny;
@@ -407,8 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
       tc::bulk_commit_wait_read();  // staging must outlive the copies' reads
     }
-    return;
-  }
+  } else {
   int64_t gv = gv0;
   const int nel = xw * C;
   const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
@@ -430,6 +456,18 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
       A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
     }
   }
+  }  // lane-parallel path
+  }  // yy < ny
+  // all TMEM reads and bulk-copy reads of the staging are done before the
+  // next tile's MMAs and operand stores reuse them
+  if (PERSIST && next_tile < A.n_tiles) {
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  tile_g = next_tile;
+  }  // tile loop
+  if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
 }
 
 template <int CM>
@@ -437,11 +475,30 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = TcShape<CM>;
   // never more than two CTAs per SM: each holds 256 of the 512 TMEM columns
   constexpr int smem = S::kSmem > 80 * 1024 ? S::kSmem : 80 * 1024;
-  auto kern = field == 9 ? eval_tc_kernel<CM, 9> : field == 8 ? eval_tc_kernel<CM, 8> : field == 6 ? eval_tc_kernel<CM, 6> : eval_tc_kernel<CM, 7>;
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm < 1) n_sm = 148;
+  }
+  const bool persist = (field == 6 || field == 7) && A.tile_counter &&
+                       A.n_entries < (int64_t)kPersistentBelow * n_tiles && n_tiles > 2 * n_sm;
+  auto kern = field == 9   ? eval_tc_kernel<CM, 9, false>
+              : field == 8 ? eval_tc_kernel<CM, 8, false>
+              : field == 6 ? (persist ? eval_tc_kernel<CM, 6, true> : eval_tc_kernel<CM, 6, false>)
+                           : (persist ? eval_tc_kernel<CM, 7, true> : eval_tc_kernel<CM, 7, false>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess)
     return check_launch("eval_tc_kernel attribute");
-  kern<<<n_tiles, kThreads, smem, s>>>(A);
+  // Sparse tiles (few primitives each: per-tile setup, staging latency and
+  // epilogue dominate) run persistent — two CTAs per SM, tiles handed out by
+  // A.tile_counter, the next tile's first chunk staged under the epilogue.
+  // Dense tiles run one CTA per tile (measured faster there).
+  const EvalArgs& B = A;
+  const int grid = persist ? 2 * n_sm : n_tiles;
+  if (grid < 1) return SQV_OK;
+  kern<<<grid, kThreads, smem, s>>>(B);
   count_launch();
   return check_launch("eval_tc_kernel");
 }

@@ -46,6 +46,9 @@ struct EvalArgs {
   uint8_t* labels;
   float* v_o;
   float* v_c;
+  int n_tiles;        // F * tiles per frame
+  int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
+  int64_t n_entries;  // (tile, primitive) entries of the batch
 };
 
 __global__ void prep_kernel(PrepArgs A);
