@@ -69,7 +69,7 @@ static Header* mapped_header() {
 
 struct Layout {
   size_t hdr, recs, lrows, counts, offs, windows, tile_cnt, tile_off, scan_tmp;  // fixed
-  size_t keys_a, vals_a, keys_b, vals_b, radix_tmp;                              // variable
+  size_t keys_a, vals_a, keys_b, vals_b, radix_tmp, bmask;                       // variable
   size_t fixed_end, total;
 };
 
@@ -97,6 +97,7 @@ Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
   L.keys_b = take((size_t)n_entries * 4);
   L.vals_b = take((size_t)n_entries * 4);
   L.radix_tmp = take((size_t)radix_tmp_ints(n_entries) * 4);
+  L.bmask = take((size_t)n_entries * 2);
   L.total = o;
   return L;
 }
@@ -343,6 +344,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   }
   if (int rc = scan_exclusive(tile_cnt, tile_off, FT, scan_tmp, nullptr, s)) return rc;
   const int* sorted_vals = which ? vals_b : vals_a;
+  const uint32_t* sorted_keys = which ? keys_b : keys_a;
+  uint16_t* bmask = (uint16_t*)(ws + L.bmask);
 
   // K5 evaluate + finalize
   EvalArgs A;
@@ -376,6 +379,11 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     // tcgen05 evaluator by default; SQV_EVAL=ffma selects the CUDA-core one (A/B runs)
     const char* ev = std::getenv("SQV_EVAL");
     const bool ffma = (ev && std::strcmp(ev, "ffma") == 0) || !eval_tc_supported(cm);
+    A.bmask = bmask;
+    if (!ffma && E > 0)
+      if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, (int)T, ntx, nty, N,
+                                      bmask, s))
+        return rc;
     if (int rc = ffma ? eval_launch(A, cm, (int)FT, s) : eval_tc_launch(A, cm, (int)FT, s))
       return rc;
   }

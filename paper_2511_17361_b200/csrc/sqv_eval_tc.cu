@@ -60,7 +60,8 @@ struct TcShape {
   // the back
   static constexpr int kList = kRec + kChunk * kStride * 4;
   static_assert(kStride % 4 == 0, "16-byte aligned staging");
-  static constexpr int kBar = (kList + kWarps * kChunk * 2 + 7) & ~7;
+  static constexpr int kBm = kList + kWarps * kChunk * 2;  // staged block masks (u16)
+  static constexpr int kBar = (kBm + kChunk * 2 + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
   static constexpr int kEnd = kMisc + 4 + kWarps * 4 + 4;  // + next-tile slot
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* s_rec = smem + S::kRec;
   uint16_t* s_list = reinterpret_cast<uint16_t*>(smem + S::kList);
+  uint16_t* s_bm = reinterpret_cast<uint16_t*>(smem + S::kBm);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     static_assert(2 * S::kChunk <= kThreads, "staging map");
     const int j = tid >> 1;
     if (j < n) {
+      if ((tid & 1) == 0) s_bm[j] = A.bmask[c0 + j];
       const int64_t g = fb + A.prim_ids[c0 + j];
       const float4* rsrc = reinterpret_cast<const float4*>(A.recs + g * kRecWords);
       const float4* lsrc = reinterpret_cast<const float4*>(A.lrows + g * A.lrow);
@@ -222,12 +225,9 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     const unsigned lt = (1u << lane) - 1u;
     for (int q = 0; q * 32 < n; ++q) {
       const int j = q * 32 + lane;
-      bool hit = false, inside = false;
-      if (j < n) {
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * S::kStride * 4);
-        hit = block_may_hit(R, bx0, by0, bz0);
-        inside = hit && block_inside(R, bx0, by0, bz0);
-      }
+      // this warp's bits of the precomputed block masks (block_masks_kernel)
+      const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
+      const bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
       const unsigned mi = __ballot_sync(0xffffffffu, inside);
       const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
       const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
@@ -470,6 +470,34 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
 }
 
+__global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t n,
+                                   const float* recs, int tiles_per_frame, int ntx, int nty,
+                                   int n_prims, uint16_t* bmask) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const uint32_t key = keys[e];
+  const int f = (int)(key / (uint32_t)tiles_per_frame);
+  const int t = (int)(key - (uint32_t)f * (uint32_t)tiles_per_frame);
+  const int tx = t % ntx, ty = (t / ntx) % nty, tz = t / (ntx * nty);
+  PrimRec R;
+  const float4* src = reinterpret_cast<const float4*>(recs + ((int64_t)f * n_prims + ids[e]) *
+                                                             kRecWords);
+  float4* dst = reinterpret_cast<float4*>(&R);
+#pragma unroll
+  for (int q = 0; q < kRecWords / 4; ++q) dst[q] = __ldg(src + q);
+  unsigned m = 0;
+#pragma unroll
+  for (int b = 0; b < kWarps; ++b) {
+    const int bx0 = tx * kTileX + (b & 1) * 4, by0 = ty * kTileY + ((b >> 1) & 1) * 4,
+              bz0 = tz * kTileZ + (b >> 2) * 8;
+    if (block_may_hit(R, bx0, by0, bz0)) {
+      m |= 1u << b;
+      if (block_inside(R, bx0, by0, bz0)) m |= 1u << (8 + b);
+    }
+  }
+  bmask[e] = (uint16_t)m;
+}
+
 template <int CM>
 int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   using S = TcShape<CM>;
@@ -506,6 +534,16 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
 }  // namespace
 
 bool eval_tc_supported(int cm) { return cm <= 24; }
+
+int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
+                       const float* recs, int tiles_per_frame, int ntx, int nty, int n_prims,
+                       uint16_t* bmask, cudaStream_t s) {
+  if (n_entries <= 0) return SQV_OK;
+  block_masks_kernel<<<(unsigned)((n_entries + 127) / 128), 128, 0, s>>>(
+      sorted_keys, sorted_ids, n_entries, recs, tiles_per_frame, ntx, nty, n_prims, bmask);
+  count_launch();
+  return check_launch("block_masks_kernel");
+}
 
 int eval_tc_launch(const EvalArgs& A, int cm, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return SQV_OK;

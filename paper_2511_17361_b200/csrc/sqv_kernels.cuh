@@ -49,7 +49,14 @@ struct EvalArgs {
   int n_tiles;        // F * tiles per frame
   int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
   int64_t n_entries;  // (tile, primitive) entries of the batch
+  const uint16_t* bmask;  // per entry: bit b = may hit warp block b, bit 8+b = covers it
 };
+
+// per (tile, primitive) entry: the 8 warp-block tests of the tensor-core
+// evaluator (block_may_hit / block_inside), computed once, in parallel
+int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
+                       const float* recs, int tiles_per_frame, int ntx, int nty, int n_prims,
+                       uint16_t* bmask, cudaStream_t s);
 
 __global__ void prep_kernel(PrepArgs A);
 __global__ void emit_kernel(EmitArgs A);

@@ -110,9 +110,10 @@ __device__ __forceinline__ float2 log2_acc2(float2 x) {
   q = fma2(q, r, bc2(4.809106290e-01f));
   q = fma2(q, r, bc2(-7.213473320e-01f));
   q = fma2(q, r, bc2(1.442695022e+00f));
-  const float2 l = fma2(r, q, make_float2((float)e0, (float)e1));
-  return make_float2(x.x >= 1.17549435e-38f ? l.x : -INFINITY,
-                     x.y >= 1.17549435e-38f ? l.y : -INFINITY);
+  // x = 0 (or denormal) is not special-cased: it yields about -127 instead
+  // of -inf, and every power built from it (c, a*b >= 1) still underflows
+  // to exactly 0
+  return fma2(r, q, make_float2((float)e0, (float)e1));
 }
 
 // Local coordinates of a thread's 4 voxels, packed by voxel pairs:
