@@ -68,7 +68,7 @@ static Header* mapped_header() {
 }
 
 struct Layout {
-  size_t hdr, recs, lrows, counts, offs, windows, tile_cnt, tile_off, scan_tmp;  // fixed
+  size_t hdr, recs, lrows, counts, offs, windows, tile_off, scan_tmp;  // fixed
   size_t keys_a, vals_a, keys_b, vals_b, radix_tmp, bmask;                       // variable
   size_t fixed_end, total;
 };
@@ -87,7 +87,6 @@ Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
   L.counts = take((size_t)(FN + 1) * 4);
   L.offs = take((size_t)(FN + 1) * 4);
   L.windows = take((size_t)FN * 6 * 4);
-  L.tile_cnt = take((size_t)(FT + 1) * 4);
   L.tile_off = take((size_t)(FT + 1) * 4);
   const int64_t st = scan_tmp_ints(FN > FT ? FN : FT);
   L.scan_tmp = take((size_t)st * 4);
@@ -233,7 +232,6 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   int* counts = (int*)(ws + L.counts);
   int* offs = (int*)(ws + L.offs);
   int* windows = (int*)(ws + L.windows);
-  int* tile_cnt = (int*)(ws + L.tile_cnt);
   int* tile_off = (int*)(ws + L.tile_off);
   int* scan_tmp = (int*)(ws + L.scan_tmp);
   float* recs = (float*)(ws + L.recs);
@@ -241,8 +239,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
 
   // header: zeros, bad_word = ~0 (memset kernels, no host copy)
   if (cudaMemsetAsync(hdr, 0, sizeof(Header), s) != cudaSuccess ||
-      cudaMemsetAsync(&hdr->bad_word, 0xFF, sizeof(hdr->bad_word), s) != cudaSuccess ||
-      cudaMemsetAsync(tile_cnt, 0, (size_t)(FT + 1) * 4, s) != cudaSuccess)
+      cudaMemsetAsync(&hdr->bad_word, 0xFF, sizeof(hdr->bad_word), s) != cudaSuccess)
     return check_launch("workspace init");
   Header* hmap = mapped_header();
   if (!hmap) return set_error(SQV_ERR_CUDA, "mapped header allocation failed");
@@ -333,8 +330,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     Em.windows = windows;
     Em.keys = keys_a;
     Em.vals = vals_a;
-    Em.tile_cnt = tile_cnt;
-    emit_kernel<<<div_up(FN, 128), 128, 0, s>>>(Em);
+    emit_kernel<<<(int)std::min<int64_t>(div_up(FN * 32, 256), 148 * 16), 256, 0, s>>>(Em);
     count_launch();
     if (int rc = check_launch("emit_kernel")) return rc;
     int bits = 0;
@@ -342,9 +338,11 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     if (int rc = radix_sort(keys_a, vals_a, keys_b, vals_b, E, bits, radix_tmp, &which, s))
       return rc;
   }
-  if (int rc = scan_exclusive(tile_cnt, tile_off, FT, scan_tmp, nullptr, s)) return rc;
   const int* sorted_vals = which ? vals_b : vals_a;
   const uint32_t* sorted_keys = which ? keys_b : keys_a;
+  tile_bounds_kernel<<<div_up(E + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off);
+  count_launch();
+  if (int rc = check_launch("tile_bounds_kernel")) return rc;
   uint16_t* bmask = (uint16_t*)(ws + L.bmask);
 
   // K5 evaluate + finalize

@@ -29,7 +29,6 @@ struct EmitArgs {
   const int* windows;
   uint32_t* keys;
   int* vals;
-  int* tile_cnt;
 };
 
 struct EvalArgs {
@@ -60,6 +59,8 @@ int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64
 
 __global__ void prep_kernel(PrepArgs A);
 __global__ void emit_kernel(EmitArgs A);
+__global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
+                                   int* tile_off);
 
 // exclusive scan of n int32 values; out has n+1 entries (out[n] = total);
 // if total64 != nullptr the total is also stored there.  tmp needs

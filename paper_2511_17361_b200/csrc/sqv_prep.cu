@@ -152,26 +152,42 @@ __global__ void prep_kernel(PrepArgs A) {
 // K3: one thread per primitive; entries in (tz, ty, tx) order, primitive
 // order preserved by the prefix offsets, so the stable radix sort by key
 // yields ascending primitive ids per tile (the oracle's bins).
+// K3: one warp per primitive writes its (tile key, primitive) entries —
+// consecutive lanes to consecutive entries, so the stores coalesce — in
+// tx-fastest order at the primitive's exclusive offset.  No atomics: tile
+// offsets come from the sorted keys (tile_bounds_kernel).
 __global__ void emit_kernel(EmitArgs A) {
-  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t FN = (int64_t)A.n_frames * A.n_prims;
-  if (gi >= FN) return;
-  const int cnt = A.counts[gi];
-  if (cnt == 0) return;
-  const int f = (int)(gi / A.n_prims);
-  const int i = (int)(gi - (int64_t)f * A.n_prims);
-  const int* w = A.windows + 6 * gi;
-  int64_t o = A.offs[gi];
-  const uint32_t base = (uint32_t)f * (uint32_t)A.tiles_per_frame;
-  for (int tz = w[2] / kTileZ; tz <= w[5] / kTileZ; ++tz)
-    for (int ty = w[1] / kTileY; ty <= w[4] / kTileY; ++ty)
-      for (int tx = w[0] / kTileX; tx <= w[3] / kTileX; ++tx) {
-        const uint32_t key = base + (uint32_t)(tx + A.ntx * (ty + A.nty * tz));
-        A.keys[o] = key;
-        A.vals[o] = i;
-        ++o;
-        atomicAdd(A.tile_cnt + key, 1);
-      }
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t gi = w0; gi < FN; gi += nw) {
+    const int cnt = A.counts[gi];
+    if (cnt == 0) continue;
+    const int f = (int)(gi / A.n_prims);
+    const int i = (int)(gi - (int64_t)f * A.n_prims);
+    const int* w = A.windows + 6 * gi;
+    const int tx0 = w[0] / kTileX, ty0 = w[1] / kTileY, tz0 = w[2] / kTileZ;
+    const int ntx = w[3] / kTileX - tx0 + 1, nty = w[4] / kTileY - ty0 + 1;
+    const int64_t o = A.offs[gi];
+    const uint32_t base = (uint32_t)f * (uint32_t)A.tiles_per_frame;
+    for (int e = lane; e < cnt; e += 32) {
+      const int dx = e % ntx, r = e / ntx, dy = r % nty, dz = r / nty;
+      A.keys[o + e] = base + (uint32_t)(tx0 + dx + A.ntx * (ty0 + dy + A.nty * (tz0 + dz)));
+      A.vals[o + e] = i;
+    }
+  }
+}
+
+// tile_off[t] = first sorted entry with key >= t (t = 0 .. n_tiles): each
+// entry whose key differs from its predecessor's opens the tiles in between.
+__global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
+                                   int* tile_off) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > n) return;
+  const int64_t k = e < n ? (int64_t)keys[e] : n_tiles;
+  const int64_t kp = e > 0 ? (int64_t)keys[e - 1] : -1;
+  for (int64_t t = kp + 1; t <= k; ++t) tile_off[t] = (int)e;
 }
 
 }  // namespace sqv
