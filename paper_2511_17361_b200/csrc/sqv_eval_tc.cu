@@ -470,6 +470,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// Per (tile, primitive) entry: which of the tile's 8 warp blocks the
+// primitive may reach (bits 0-7) and which blocks lie entirely inside its
+// window (bits 8-15).  The cull decisions are those of block_may_hit (window
+// overlap, the Chebyshev box bound, the nearest-corner field bound, all
+// conservative); the shared parts are computed once per entry (local block
+// centres differ by fixed lattice steps), and a block whose nearest local
+// corner is deep inside — (2^b + 1) max|x'|^c well below kFCut — is marked
+// without the 8-MUFU field test.  A "hit" that could have been culled only
+// costs evaluation work: those pairs still get w = 0 exactly.
 __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t n,
                                    const float* recs, int tiles_per_frame, int ntx, int nty,
                                    int n_prims, uint16_t* bmask) {
@@ -485,14 +494,48 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
   float4* dst = reinterpret_cast<float4*>(&R);
 #pragma unroll
   for (int q = 0; q < kRecWords / 4; ++q) dst[q] = __ldg(src + q);
+  const int x0 = tx * kTileX, y0 = ty * kTileY, z0 = tz * kTileZ;
+  float ex[3], ey[3], ez[3], c0[3], h[3];
+  const float kx = (float)x0 + 1.5f - R.cx, ky = (float)y0 + 1.5f - R.cy,
+              kz = (float)z0 + 3.5f - R.cz;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    ex[r] = R.HL[3 * r].x + R.HL[3 * r].y;
+    ey[r] = R.HL[3 * r + 1].x + R.HL[3 * r + 1].y;
+    ez[r] = R.HL[3 * r + 2].x + R.HL[3 * r + 2].y;
+    c0[r] = fmaf(kz, ez[r], fmaf(ky, ey[r], fmaf(kx, ex[r], R.G[r].x + R.G[r].y)));
+    h[r] = 1.5f * fabsf(ex[r]) + 1.5f * fabsf(ey[r]) + 3.5f * fabsf(ez[r]);
+  }
+  // sure-hit radius: (2^b + 1) M^c <= 0.5 kFCut  <=>  M <= (0.5 kFCut / (2^b + 1))^(1/c)
+  const float inv_c = 1.0f / R.c;
+  const float sure = ex2(inv_c * lg2(0.5f * kFCut / (ex2(R.b) + 1.0f)));
   unsigned m = 0;
 #pragma unroll
-  for (int b = 0; b < kWarps; ++b) {
-    const int bx0 = tx * kTileX + (b & 1) * 4, by0 = ty * kTileY + ((b >> 1) & 1) * 4,
-              bz0 = tz * kTileZ + (b >> 2) * 8;
-    if (block_may_hit(R, bx0, by0, bz0)) {
-      m |= 1u << b;
-      if (block_inside(R, bx0, by0, bz0)) m |= 1u << (8 + b);
+  for (int bb = 0; bb < kWarps; ++bb) {
+    const int dx = (bb & 1) * 4, dy = ((bb >> 1) & 1) * 4, dz = (bb >> 2) * 8;
+    const int bx0 = x0 + dx, by0 = y0 + dy, bz0 = z0 + dz;
+    if (bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
+        bz0 + 7 < R.lo[2] || bz0 > R.hi[2])
+      continue;
+    float mm[3], dmax = -1.0f, slack = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const float c = c0[r] + ((float)dx * ex[r] + (float)dy * ey[r] + (float)dz * ez[r]);
+      mm[r] = fabsf(c) - h[r];
+      dmax = fmaxf(dmax, mm[r]);
+      slack += fabsf(c) + h[r];
+    }
+    const float eps = 1e-4f * slack;  // FP32 error of c, h (incl. the stepped centres)
+    if (dmax > R.mcut + eps) continue;
+    bool hit = dmax <= sure;
+    if (!hit) {
+      const float F = field_F(fmaxf(mm[0] - eps, 0.0f), fmaxf(mm[1] - eps, 0.0f),
+                              fmaxf(mm[2] - eps, 0.0f), R.a, R.b, R.c);
+      hit = F < 1.02f * kFCut;
+    }
+    if (hit) {
+      m |= 1u << bb;
+      if (block_inside(R, bx0, by0, bz0)) m |= 1u << (8 + bb);
     }
   }
   bmask[e] = (uint16_t)m;
