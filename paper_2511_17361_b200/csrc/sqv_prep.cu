@@ -43,10 +43,9 @@ __device__ inline void split_row(const double v[3], double g, float2 hl[3], floa
                     (float)(g - gh));
 }
 
-__global__ void prep_kernel(PrepArgs A) {
-  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t FN = (int64_t)A.n_frames * A.n_prims;
-  if (gi >= FN) return;
+// Primitive gi of the batch: validation, window, tile count, record, class
+// weights.  Returns its in-window voxel count (algorithmic pairs).
+__device__ __forceinline__ int64_t prep_prim(const PrepArgs& A, int64_t gi) {
   const int f = (int)(gi / A.n_prims);
   const int i = (int)(gi - (int64_t)f * A.n_prims);
   const int C = A.n_classes;
@@ -57,8 +56,9 @@ __global__ void prep_kernel(PrepArgs A) {
   rec.lo[0] = rec.lo[1] = rec.lo[2] = 1;
   rec.hi[0] = rec.hi[1] = rec.hi[2] = 0;
   int count = 0;
+  int64_t vol = 0;  // in-window voxels (algorithmic pairs) of this primitive
   float* lrow = A.lrows + gi * A.lrow;
-  for (int k = 0; k < A.lrow; ++k) lrow[k] = 0.0f;
+  bool lrow_done = false;
 
   const bool valid_slot = !A.n_valid || i < A.n_valid[f];
   if (valid_slot) {
@@ -89,7 +89,7 @@ __global__ void prep_kernel(PrepArgs A) {
       }
       if (!empty && P.sigma > 0.0) {  // sigma = 0 primitives are skipped
         int ilo[3], ihi[3];
-        int64_t vol = 1;
+        vol = 1;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           ilo[k] = (int)lo[k];
@@ -100,7 +100,6 @@ __global__ void prep_kernel(PrepArgs A) {
         }
         count = (ihi[0] / kTileX - ilo[0] / kTileX + 1) * (ihi[1] / kTileY - ilo[1] / kTileY + 1) *
                 (ihi[2] / kTileZ - ilo[2] / kTileZ + 1);
-        atomicAdd(A.n_pairs, (unsigned long long)vol);
         // ---- evaluation record ----
         // reference voxel: the centre voxel clamped into the window, so that
         // lattice offsets k = idx - cref stay small integers.
@@ -121,7 +120,8 @@ __global__ void prep_kernel(PrepArgs A) {
         rec.b = (float)(P.e2 / P.e1);
         rec.c = (float)(2.0 / P.e1);
         // F >= max(|x'|)^(2/e1): cull when max|x'| > kFCut^(e1/2) (+0.1% margin)
-        rec.mcut = __double2float_ru(pow((double)kFCut, 0.5 * P.e1) * 1.001);
+        // (exp2 of 0.5 e1 log2(kFCut); the 0.1% margin dwarfs its ulp error)
+        rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * 6.448512845609085) * 1.001);
         rec.cx = (float)cref[0];
         rec.cy = (float)cref[1];
         rec.cz = (float)cref[2];
@@ -135,10 +135,14 @@ __global__ void prep_kernel(PrepArgs A) {
         } else {
           for (int k = 0; k < C; ++k) lrow[k] = (float)logits[k];
         }
+        for (int k = C; k < A.lrow; ++k) lrow[k] = 0.0f;
         lrow[A.cm] = (float)P.sigma;
+        lrow_done = true;
       }
     }
   }
+  if (!lrow_done)
+    for (int k = 0; k < A.lrow; ++k) lrow[k] = 0.0f;
   reinterpret_cast<PrimRec*>(A.recs)[gi] = rec;
   A.counts[gi] = count;
   int* win = A.windows + 6 * gi;
@@ -147,6 +151,18 @@ __global__ void prep_kernel(PrepArgs A) {
     win[k] = rec.lo[k];
     win[3 + k] = rec.hi[k];
   }
+  return vol;
+}
+
+__global__ void prep_kernel(PrepArgs A) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t FN = (int64_t)A.n_frames * A.n_prims;
+  unsigned long long v = gi < FN ? (unsigned long long)prep_prim(A, gi) : 0ull;
+  // one atomic per warp for the algorithmic pair count (not one per primitive
+  // on a single address)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.n_pairs, v);
 }
 
 // K3: one thread per primitive; entries in (tz, ty, tx) order, primitive
