@@ -29,6 +29,7 @@
 #include "sqv_pair.cuh"
 #include "sqv_tc.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace sqv {
@@ -195,277 +196,277 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   int tile_g = blockIdx.x;
   bool prefetched = false;
   while (tile_g < A.n_tiles) {
-  const int f = tile_g / A.tiles_per_frame;
-  const int t = tile_g - f * A.tiles_per_frame;
-  const int tx = t % A.ntx;
-  const int ty = (t / A.ntx) % A.nty;
-  const int tz = t / (A.ntx * A.nty);
-  const int bx0 = tx * kTileX + (warp & 1) * 4;
-  const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
-  const int bz0 = tz * kTileZ + (warp >> 2) * 8;
-  const int x = bx0 + (lane & 3);
-  const int y = by0 + ((lane >> 2) & 3);
-  const int z0 = bz0 + (lane >> 4) * 4;
-  kk = 0;
-  groups = 0;
-  // claim the next tile now; the result is only needed at the epilogue
-  const int claimed = (PERSIST && tid == 0) ? atomicAdd(A.tile_counter, 1) : 0;
-  const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
-  const int64_t fbase = (int64_t)f * A.n_prims;
-  for (int c0 = beg; c0 < end; c0 += S::kChunk) {
-    const int n = min(S::kChunk, end - c0);
-    if (!(prefetched && c0 == beg)) {
-      __syncthreads();  // every warp is done with the previous chunk
-      stage_chunk(fbase, c0, n);
-    }
-    tc::cp_async_wait_all();
-    __syncthreads();
-    uint16_t* lst = s_list + warp * S::kChunk;
-    int n_in = 0, n_part = 0;  // warp-uniform list lengths
-    const unsigned lt = (1u << lane) - 1u;
-    for (int q = 0; q * 32 < n; ++q) {
-      const int j = q * 32 + lane;
-      // this warp's bits of the precomputed block masks (block_masks_kernel)
-      const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
-      const bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
-      const unsigned mi = __ballot_sync(0xffffffffu, inside);
-      const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
-      const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
-      if (inside) lst[n_in + __popc(mi & lt)] = off;
-      if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = off;
-      n_in += __popc(mi);
-      n_part += __popc(mp);
-    }
-    __syncwarp();
-    auto push = [&](const float(&w)[kVPT], float cw) {
-      if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
-      store_k(kk, w, cw);
-      if (++kk == kK) issue();
-    };
-    // class weight n = lane (sigma at CM), zero beyond
-    auto class_weight = [&](int off) {
-      return lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane]
-                             : 0.0f;
-    };
-    // whole-block primitives first (no per-voxel window test), then the rest,
-    // each in ascending primitive order
-    const int n_tot = n_in + n_part;
-    auto off_at = [&](int k) {
-      return (int)(k < n_in ? lst[k] : lst[S::kChunk - 1 - (k - n_in)]) << 4;
-    };
-    if constexpr (FIELD == 6 || FIELD == 7) {
-      // two-stage software pipeline: the logs of primitive k interleave with
-      // the exps of primitive k-1 (independent chains for the latency-bound
-      // SFU/FMA mix); the hand-off lives in registers
-      auto step = [&](int k, int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-        nxt.cw = class_weight(off);
-        const bool part = k >= n_in;
-        if (wants_acc<FIELD>(R)) {
-          if (part) {
-            stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
-            stage_exps<1>(cur, w);
-          } else {
-            stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
-            stage_exps<2>(cur, w);
-          }
-        } else {
-          if (part) {
-            stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
-            stage_exps<3>(cur, w);
-          } else {
-            stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
-            stage_exps<4>(cur, w);
-          }
-        }
+    const int f = tile_g / A.tiles_per_frame;
+    const int t = tile_g - f * A.tiles_per_frame;
+    const int tx = t % A.ntx;
+    const int ty = (t / A.ntx) % A.nty;
+    const int tz = t / (A.ntx * A.nty);
+    const int bx0 = tx * kTileX + (warp & 1) * 4;
+    const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
+    const int bz0 = tz * kTileZ + (warp >> 2) * 8;
+    const int x = bx0 + (lane & 3);
+    const int y = by0 + ((lane >> 2) & 3);
+    const int z0 = bz0 + (lane >> 4) * 4;
+    kk = 0;
+    groups = 0;
+    // claim the next tile now; the result is only needed at the epilogue
+    const int claimed = (PERSIST && tid == 0) ? atomicAdd(A.tile_counter, 1) : 0;
+    const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
+    const int64_t fbase = (int64_t)f * A.n_prims;
+    for (int c0 = beg; c0 < end; c0 += S::kChunk) {
+      const int n = min(S::kChunk, end - c0);
+      if (!(prefetched && c0 == beg)) {
+        __syncthreads();  // every warp is done with the previous chunk
+        stage_chunk(fbase, c0, n);
+      }
+      tc::cp_async_wait_all();
+      __syncthreads();
+      uint16_t* lst = s_list + warp * S::kChunk;
+      int n_in = 0, n_part = 0;  // warp-uniform list lengths
+      const unsigned lt = (1u << lane) - 1u;
+      for (int q = 0; q * 32 < n; ++q) {
+        const int j = q * 32 + lane;
+        // this warp's bits of the precomputed block masks (block_masks_kernel)
+        const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
+        const bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
+        const unsigned mi = __ballot_sync(0xffffffffu, inside);
+        const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
+        const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
+        if (inside) lst[n_in + __popc(mi & lt)] = off;
+        if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = off;
+        n_in += __popc(mi);
+        n_part += __popc(mp);
+      }
+      __syncwarp();
+      auto push = [&](const float(&w)[kVPT], float cw) {
+        if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
+        store_k(kk, w, cw);
+        if (++kk == kK) issue();
       };
-      if (n_tot > 0) {
-        PairState s0, s1;
-        float w[kVPT];
-        {
-          const int off = off_at(0);
+      // class weight n = lane (sigma at CM), zero beyond
+      auto class_weight = [&](int off) {
+        return lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane]
+                               : 0.0f;
+      };
+      // whole-block primitives first (no per-voxel window test), then the rest,
+      // each in ascending primitive order
+      const int n_tot = n_in + n_part;
+      auto off_at = [&](int k) {
+        return (int)(k < n_in ? lst[k] : lst[S::kChunk - 1 - (k - n_in)]) << 4;
+      };
+      if constexpr (FIELD == 6 || FIELD == 7) {
+        // two-stage software pipeline: the logs of primitive k interleave with
+        // the exps of primitive k-1 (independent chains for the latency-bound
+        // SFU/FMA mix); the hand-off lives in registers
+        auto step = [&](int k, int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
           const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-          s0.cw = class_weight(off);
+          nxt.cw = class_weight(off);
+          const bool part = k >= n_in;
           if (wants_acc<FIELD>(R)) {
-            if (n_in == 0)
-              stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
-            else
-              stage_logs<FIELD == 6, false, true>(R, x, y, z0, s0);
+            if (part) {
+              stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
+              stage_exps<1>(cur, w);
+            } else {
+              stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
+              stage_exps<2>(cur, w);
+            }
           } else {
-            if (n_in == 0)
-              stage_logs<FIELD == 6, true, false>(R, x, y, z0, s0);
-            else
-              stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
+            if (part) {
+              stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
+              stage_exps<3>(cur, w);
+            } else {
+              stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
+              stage_exps<4>(cur, w);
+            }
+          }
+        };
+        if (n_tot > 0) {
+          PairState s0, s1;
+          float w[kVPT];
+          {
+            const int off = off_at(0);
+            const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+            s0.cw = class_weight(off);
+            if (wants_acc<FIELD>(R)) {
+              if (n_in == 0)
+                stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
+              else
+                stage_logs<FIELD == 6, false, true>(R, x, y, z0, s0);
+            } else {
+              if (n_in == 0)
+                stage_logs<FIELD == 6, true, false>(R, x, y, z0, s0);
+              else
+                stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
+            }
+          }
+          // list entries are read one step ahead (past the end: harmless reads
+          // inside the CTA's shared memory, discarded)
+          int k = 1, off = off_at(1);
+          for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
+            const int off1 = off_at(k + 1);
+            step(k, off, s1, s0, w);
+            push(w, s0.cw);
+            off = off_at(k + 2);
+            step(k + 1, off1, s0, s1, w);
+            push(w, s1.cw);
+          }
+          if (k < n_tot) {
+            step(k, off, s1, s0, w);
+            push(w, s0.cw);
+            stage_exps(s1, w);
+            push(w, s1.cw);
+          } else {
+            stage_exps(s0, w);
+            push(w, s0.cw);
           }
         }
-        // list entries are read one step ahead (past the end: harmless reads
-        // inside the CTA's shared memory, discarded)
-        int k = 1, off = off_at(1);
-        for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
-          const int off1 = off_at(k + 1);
-          step(k, off, s1, s0, w);
-          push(w, s0.cw);
-          off = off_at(k + 2);
-          step(k + 1, off1, s0, s1, w);
-          push(w, s1.cw);
-        }
-        if (k < n_tot) {
-          step(k, off, s1, s0, w);
-          push(w, s0.cw);
-          stage_exps(s1, w);
-          push(w, s1.cw);
-        } else {
-          stage_exps(s0, w);
-          push(w, s0.cw);
-        }
-      }
-    } else {
-      for (int k = 0; k < n_tot; ++k) {
-        const int off = off_at(k);
-        const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-        float w[kVPT];
-        pair_weights<FIELD, true>(R, x, y, z0, w);
-        push(w, class_weight(off));
-      }
-    }
-  }
-  if (kk > 0) {  // close the last K step with zero columns
-    const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = kk; k < kK; ++k) store_k(k, zw, 0.0f);
-    issue();
-  }
-  wait_free();
-  if (lane == 0) s_has[warp] = groups > 0;
-  // next tile (one atomic per CTA), published by the barrier below
-  if (PERSIST && tid == 0) *s_next = (int)gridDim.x + claimed;
-  tc::fence_before_sync();
-  __syncthreads();  // all MMAs complete; operand smem is free for staging
-  tc::fence_after_sync();
-  const int next_tile = PERSIST ? *s_next : A.n_tiles;
-  prefetched = false;
-  if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
-    const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
-    if (ne > nb) {
-      const int nf = next_tile / A.tiles_per_frame;
-      stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
-      prefetched = true;
-    }
-  }
-
-  // ---- epilogue: TMEM -> finalize -> staged coalesced stores -------------
-  const int C = A.n_classes;
-  const int nx = A.nx, ny = A.ny, nz = A.nz;
-  const int x_t = tx * kTileX, y_t = ty * kTileY, z_t = tz * kTileZ;
-  const int zpc = 64 * C + 8;                          // padded z pitches
-  constexpr int zpo = 72;
-  float* s_vc = reinterpret_cast<float*>(smem);        // [16][zpc]
-  float* s_vo = s_vc + 16 * zpc;                       // [16][zpo]
-  uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 16 * zpo);
-  const int qd = warp & 3;  // TMEM lane quarter this warp may access
-#pragma unroll 1
-  for (int i = 0; i < 4; ++i) {
-    const int mb = (warp & 4) + i;  // M block (= producing warp)
-    float vals[32];
-    if (s_has[mb]) {
-      tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN), vals);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
-    }
-    // TMEM lane 32*qd + lane = row = src_lane*4 + v of block mb
-    const int src = qd * 8 + (lane >> 2), v = lane & 3;
-    const int vx = (mb & 1) * 4 + (src & 3);
-    const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
-    const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
-    const int loc = vx + kTileX * vy;  // within the z layer
-    int best = 0;
-    float bv = vals[0];
-#pragma unroll
-    for (int k = 1; k < CM; ++k)
-      if (k < C && vals[k] > bv) {
-        bv = vals[k];
-        best = k;
-      }
-    const float vo = vals[CM];
-    if (A.v_c) {
-#pragma unroll
-      for (int k = 0; k < CM; ++k)
-        if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
-    }
-    s_vo[vz * zpo + loc] = vo;
-    s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
-  }
-  tc::fence_proxy_async_smem();  // staging -> visible to the bulk-copy engine
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  // rows of 8 voxels: this warp owns y row y_t + warp (8 warps = the tile's
-  // 8 y rows) for every z layer, so the row base just steps by nx*ny
-  const int64_t V = (int64_t)nx * ny * nz;
-  const int xw = min(kTileX, nx - x_t);
-  const int yy = y_t + warp;
-  if (yy < ny) {
-  const int zend = min(kTileZ, nz - z_t);
-  const int64_t gv0 = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
-  const int64_t zstep = (int64_t)nx * ny;
-  // Full rows whose global addresses are 16-byte aligned go out as bulk
-  // async copies (one lane per z layer: the v_c row of 8*C floats and the
-  // v_o row of 8 floats) and one 8-byte label store; the rest take the
-  // lane-parallel path.  Alignment is uniform per launch (row and layer
-  // strides), so the choice is warp-uniform.
-  const bool full = xw == kTileX;
-  const bool vc_bulk = !A.v_c || (full && ((nx * C) & 3) == 0 && ((V * C) & 3) == 0 &&
-                                  (reinterpret_cast<uintptr_t>(A.v_c) & 15) == 0);
-  const bool vo_bulk = !A.v_o || (full && (nx & 3) == 0 && (V & 3) == 0 &&
-                                  (reinterpret_cast<uintptr_t>(A.v_o) & 15) == 0);
-  const bool lab8 = full && (nx & 7) == 0 && (V & 7) == 0 &&
-                    (reinterpret_cast<uintptr_t>(A.labels) & 7) == 0;
-  if (vc_bulk && vo_bulk && lab8) {
-    if (lane < zend) {
-      const int zl = lane;
-      const int64_t gv = gv0 + zl * zstep;
-      if (A.v_c)
-        tc::bulk_store(A.v_c + gv * C, tc::smem_u32(s_vc + zl * zpc + warp * kTileX * C),
-                       (uint32_t)(kTileX * C * 4));
-      if (A.v_o)
-        tc::bulk_store(A.v_o + gv, tc::smem_u32(s_vo + zl * zpo + warp * kTileX),
-                       (uint32_t)(kTileX * 4));
-      *reinterpret_cast<uint2*>(A.labels + gv) =
-          *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
-      tc::bulk_commit_wait_read();  // staging must outlive the copies' reads
-    }
-  } else {
-  int64_t gv = gv0;
-  const int nel = xw * C;
-  const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
-  const int nel4 = nel >> 2;
-  for (int zl = 0; zl < zend; ++zl, gv += zstep) {
-    if (A.v_c) {
-      const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
-      float* dst = A.v_c + gv * C;
-      if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        const float4* s4 = reinterpret_cast<const float4*>(src);
-        float4* d4 = reinterpret_cast<float4*>(dst);
-        for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
       } else {
-        for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+        for (int k = 0; k < n_tot; ++k) {
+          const int off = off_at(k);
+          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+          float w[kVPT];
+          pair_weights<FIELD, true>(R, x, y, z0, w);
+          push(w, class_weight(off));
+        }
       }
     }
-    if (lane < xw) {
-      if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
-      A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
+    if (kk > 0) {  // close the last K step with zero columns
+      const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = kk; k < kK; ++k) store_k(k, zw, 0.0f);
+      issue();
     }
-  }
-  }  // lane-parallel path
-  }  // yy < ny
-  // all TMEM reads and bulk-copy reads of the staging are done before the
-  // next tile's MMAs and operand stores reuse them
-  if (PERSIST && next_tile < A.n_tiles) {
+    wait_free();
+    if (lane == 0) s_has[warp] = groups > 0;
+    // next tile (one atomic per CTA), published by the barrier below
+    if (PERSIST && tid == 0) *s_next = (int)gridDim.x + claimed;
+    tc::fence_before_sync();
+    __syncthreads();  // all MMAs complete; operand smem is free for staging
+    tc::fence_after_sync();
+    const int next_tile = PERSIST ? *s_next : A.n_tiles;
+    prefetched = false;
+    if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
+      const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
+      if (ne > nb) {
+        const int nf = next_tile / A.tiles_per_frame;
+        stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
+        prefetched = true;
+      }
+    }
+
+    // ---- epilogue: TMEM -> finalize -> staged coalesced stores -------------
+    const int C = A.n_classes;
+    const int nx = A.nx, ny = A.ny, nz = A.nz;
+    const int x_t = tx * kTileX, y_t = ty * kTileY, z_t = tz * kTileZ;
+    const int zpc = 64 * C + 8;                          // padded z pitches
+    constexpr int zpo = 72;
+    float* s_vc = reinterpret_cast<float*>(smem);        // [16][zpc]
+    float* s_vo = s_vc + 16 * zpc;                       // [16][zpo]
+    uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 16 * zpo);
+    const int qd = warp & 3;  // TMEM lane quarter this warp may access
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      const int mb = (warp & 4) + i;  // M block (= producing warp)
+      float vals[32];
+      if (s_has[mb]) {
+        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN), vals);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
+      }
+      // TMEM lane 32*qd + lane = row = src_lane*4 + v of block mb
+      const int src = qd * 8 + (lane >> 2), v = lane & 3;
+      const int vx = (mb & 1) * 4 + (src & 3);
+      const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
+      const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
+      const int loc = vx + kTileX * vy;  // within the z layer
+      int best = 0;
+      float bv = vals[0];
+#pragma unroll
+      for (int k = 1; k < CM; ++k)
+        if (k < C && vals[k] > bv) {
+          bv = vals[k];
+          best = k;
+        }
+      const float vo = vals[CM];
+      if (A.v_c) {
+#pragma unroll
+        for (int k = 0; k < CM; ++k)
+          if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
+      }
+      s_vo[vz * zpo + loc] = vo;
+      s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
+    }
+    tc::fence_proxy_async_smem();  // staging -> visible to the bulk-copy engine
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-  }
-  tile_g = next_tile;
+    // rows of 8 voxels: this warp owns y row y_t + warp (8 warps = the tile's
+    // 8 y rows) for every z layer, so the row base just steps by nx*ny
+    const int64_t V = (int64_t)nx * ny * nz;
+    const int xw = min(kTileX, nx - x_t);
+    const int yy = y_t + warp;
+    if (yy < ny) {
+    const int zend = min(kTileZ, nz - z_t);
+    const int64_t gv0 = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
+    const int64_t zstep = (int64_t)nx * ny;
+    // Full rows whose global addresses are 16-byte aligned go out as bulk
+    // async copies (one lane per z layer: the v_c row of 8*C floats and the
+    // v_o row of 8 floats) and one 8-byte label store; the rest take the
+    // lane-parallel path.  Alignment is uniform per launch (row and layer
+    // strides), so the choice is warp-uniform.
+    const bool full = xw == kTileX;
+    const bool vc_bulk = !A.v_c || (full && ((nx * C) & 3) == 0 && ((V * C) & 3) == 0 &&
+                                    (reinterpret_cast<uintptr_t>(A.v_c) & 15) == 0);
+    const bool vo_bulk = !A.v_o || (full && (nx & 3) == 0 && (V & 3) == 0 &&
+                                    (reinterpret_cast<uintptr_t>(A.v_o) & 15) == 0);
+    const bool lab8 = full && (nx & 7) == 0 && (V & 7) == 0 &&
+                      (reinterpret_cast<uintptr_t>(A.labels) & 7) == 0;
+    if (vc_bulk && vo_bulk && lab8) {
+      if (lane < zend) {
+        const int zl = lane;
+        const int64_t gv = gv0 + zl * zstep;
+        if (A.v_c)
+          tc::bulk_store(A.v_c + gv * C, tc::smem_u32(s_vc + zl * zpc + warp * kTileX * C),
+                         (uint32_t)(kTileX * C * 4));
+        if (A.v_o)
+          tc::bulk_store(A.v_o + gv, tc::smem_u32(s_vo + zl * zpo + warp * kTileX),
+                         (uint32_t)(kTileX * 4));
+        *reinterpret_cast<uint2*>(A.labels + gv) =
+            *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
+        tc::bulk_commit_wait_read();  // staging must outlive the copies' reads
+      }
+    } else {
+    int64_t gv = gv0;
+    const int nel = xw * C;
+    const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
+    const int nel4 = nel >> 2;
+    for (int zl = 0; zl < zend; ++zl, gv += zstep) {
+      if (A.v_c) {
+        const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
+        float* dst = A.v_c + gv * C;
+        if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          const float4* s4 = reinterpret_cast<const float4*>(src);
+          float4* d4 = reinterpret_cast<float4*>(dst);
+          for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
+        } else {
+          for (int e = lane; e < nel; e += 32) dst[e] = src[e];
+        }
+      }
+      if (lane < xw) {
+        if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
+        A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
+      }
+    }
+    }  // lane-parallel path
+    }  // yy < ny
+    // all TMEM reads and bulk-copy reads of the staging are done before the
+    // next tile's MMAs and operand stores reuse them
+    if (PERSIST && next_tile < A.n_tiles) {
+      tc::fence_before_sync();
+      __syncthreads();
+      tc::fence_after_sync();
+    }
+    tile_g = next_tile;
   }  // tile loop
   if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
 }
@@ -553,8 +554,10 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm < 1) n_sm = 148;
   }
-  const bool persist = (field == 6 || field == 7) && A.tile_counter &&
-                       A.n_entries < (int64_t)kPersistentBelow * n_tiles && n_tiles > 2 * n_sm;
+  bool persist = (field == 6 || field == 7) && A.tile_counter &&
+                 A.n_entries < (int64_t)kPersistentBelow * n_tiles && n_tiles > 2 * n_sm;
+  if (const char* pe = std::getenv("SQV_PERSIST"))  // tests / A-B: force 0 or 1
+    persist = (field == 6 || field == 7) && A.tile_counter && std::atoi(pe) != 0;
   auto kern = field == 9   ? eval_tc_kernel<CM, 9, false>
               : field == 8 ? eval_tc_kernel<CM, 8, false>
               : field == 6 ? (persist ? eval_tc_kernel<CM, 6, true> : eval_tc_kernel<CM, 6, false>)

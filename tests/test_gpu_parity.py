@@ -385,3 +385,22 @@ def test_degenerate_inputs_and_free_index():
     lab = np.asarray(sem.labels)
     assert lab.min() == -1 and set(np.unique(lab)) <= {-1, 1}
     assert lab[4, 4, 2] == 1
+
+
+@pytest.mark.parametrize("n_prims", [256, 2000])
+def test_persistent_and_per_tile_evaluators_bit_identical(monkeypatch, n_prims):
+    """The persistent evaluator (tile counter, prefetch under the epilogue)
+    and one CTA per tile run the same per-tile code: identical bits."""
+    P = _pkg()
+    from paper_2511_17361_b200.scenegen import gen_frames
+    spec = P.VoxelGridSpec()
+    for prec in ("strict", "fast"):
+        cfg = P.VoxelizeConfig(precision=prec)
+        b = gen_frames(31, 3, n_prims)
+        outs = []
+        for mode in ("1", "0"):
+            monkeypatch.setenv("SQV_PERSIST", mode)
+            r = P.Voxelizer(spec, cfg, 18)(b, dense=True)
+            outs.append({k: getattr(r, k).cpu().numpy() for k in ("labels", "v_o", "v_c")})
+        for k in ("labels", "v_o", "v_c"):
+            np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=f"{prec} {k}")
