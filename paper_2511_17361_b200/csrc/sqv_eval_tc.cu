@@ -264,19 +264,19 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           const bool part = k >= n_in;
           if (wants_acc<FIELD>(R)) {
             if (part) {
-              stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
               stage_exps<1>(cur, w);
+              stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
             } else {
-              stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
               stage_exps<2>(cur, w);
+              stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
             }
           } else {
             if (part) {
-              stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
               stage_exps<3>(cur, w);
+              stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
             } else {
-              stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
               stage_exps<4>(cur, w);
+              stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
             }
           }
         };
