@@ -330,7 +330,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     Em.windows = windows;
     Em.keys = keys_a;
     Em.vals = vals_a;
-    emit_kernel<<<(int)std::min<int64_t>(div_up(FN * 32, 256), 148 * 16), 256, 0, s>>>(Em);
+    emit_kernel<<<(int)div_up(FN * 32, 256), 256, 0, s>>>(Em);
     count_launch();
     if (int rc = check_launch("emit_kernel")) return rc;
     int bits = 0;
@@ -340,7 +340,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   }
   const int* sorted_vals = which ? vals_b : vals_a;
   const uint32_t* sorted_keys = which ? keys_b : keys_a;
-  tile_bounds_kernel<<<div_up(E + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off);
+  tile_bounds_kernel<<<div_up(FT + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off);
   count_launch();
   if (int rc = check_launch("tile_bounds_kernel")) return rc;
   uint16_t* bmask = (uint16_t*)(ws + L.bmask);

@@ -195,15 +195,22 @@ __global__ void emit_kernel(EmitArgs A) {
   }
 }
 
-// tile_off[t] = first sorted entry with key >= t (t = 0 .. n_tiles): each
-// entry whose key differs from its predecessor's opens the tiles in between.
+// tile_off[t] = first sorted entry with key >= t (t = 0 .. n_tiles): one
+// thread per tile, a binary search over the sorted keys (the upper levels
+// stay in L2/L1 for every thread).
 __global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
                                    int* tile_off) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e > n) return;
-  const int64_t k = e < n ? (int64_t)keys[e] : n_tiles;
-  const int64_t kp = e > 0 ? (int64_t)keys[e - 1] : -1;
-  for (int64_t t = kp + 1; t <= k; ++t) tile_off[t] = (int)e;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > n_tiles) return;
+  int64_t lo = 0, hi = n;  // first index in [lo, hi) with keys[idx] >= t
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)__ldg(keys + mid) < t)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  tile_off[t] = (int)lo;
 }
 
 }  // namespace sqv
