@@ -433,8 +433,12 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
                          (uint32_t)(kTileX * 4));
         *reinterpret_cast<uint2*>(A.labels + gv) =
             *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
-        tc::bulk_commit_wait_read();  // staging must outlive the copies' reads
       }
+      // commit + wait outside the per-lane issue (which the compiler runs as
+      // a loop over lanes): all copies are in flight before any lane waits;
+      // the staging must outlive their reads
+      __syncwarp();
+      tc::bulk_commit_wait_read();
     } else {
     int64_t gv = gv0;
     const int nel = xw * C;
