@@ -39,7 +39,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kPersistentBelow = 64;  // mean primitives per tile
 constexpr int kWarps = 8;
-constexpr int kMaxChunk = 128;  // primitives staged per chunk (smem budget: 2 CTAs/SM)
 constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
 constexpr int kN = 32;       // class weights + sigma, padded
 constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns

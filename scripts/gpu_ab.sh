@@ -1,12 +1,12 @@
-# A/B: "FIELD:EVAL:PIPE" variants -> bench eval time + config-1 precision
-# usage: bash scripts/gpu_ab.sh 6:tc:1 6:tc:0 7:tc:1
+# A/B: "FIELD:EVAL:TAG" variants (SQV_FIELD, SQV_EVAL; TAG is free text) -> bench eval
+# time + config-1 precision.  usage: bash scripts/gpu_ab.sh 6:tc:0 7:tc:0 6:ffma:0
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 for V in "$@"; do
   IFS=: read F E PP <<< "$V"
   tag=${F}_${E}_${PP}
-  SQV_FIELD=$F SQV_EVAL=$E SQV_PIPE=$PP timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_$tag.json 2>/dev/null
-  SQV_FIELD=$F SQV_EVAL=$E SQV_PIPE=$PP timeout 600 python scripts/diag_precision.py > /dev/null 2>&1; cp gpurun_out/diag_precision.json gpurun_out/ab_${tag}_prec.json
+  SQV_FIELD=$F SQV_EVAL=$E timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_$tag.json 2>/dev/null
+  SQV_FIELD=$F SQV_EVAL=$E timeout 600 python scripts/diag_precision.py > /dev/null 2>&1; cp gpurun_out/diag_precision.json gpurun_out/ab_${tag}_prec.json
   python - $tag <<'PY'
 import json,sys
 tag=sys.argv[1]
