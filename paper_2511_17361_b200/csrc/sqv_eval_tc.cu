@@ -388,9 +388,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         }
       const float vo = vals[CM];
       if (A.v_c) {
+        if ((CM & 1) == 0 && C == CM) {  // 8-byte stores: zpc and loc * C are even
+          float2* d2 = reinterpret_cast<float2*>(s_vc + vz * zpc + loc * CM);
 #pragma unroll
-        for (int k = 0; k < CM; ++k)
-          if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
+          for (int k = 0; k < CM / 2; ++k) d2[k] = make_float2(vals[2 * k], vals[2 * k + 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < CM; ++k)
+            if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
+        }
       }
       s_vo[vz * zpo + loc] = vo;
       s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
