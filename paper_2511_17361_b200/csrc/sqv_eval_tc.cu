@@ -25,460 +25,20 @@
 // its primitives in ascending order within each K step, so results are
 // deterministic.  Epilogue: tcgen05.ld (warp w reads TMEM lanes 32*(w%4)..+31)
 // -> finalize (tau, first argmax) -> staged coalesced stores.
-#include "sqv_kernels.cuh"
-#include "sqv_pair.cuh"
-#include "sqv_tc.cuh"
-
-#include <cstdlib>
-#include <type_traits>
+#include "sqv_eval_tc_impl.cuh"
 
 namespace sqv {
 
+// launch_tc<CM> is instantiated in sqv_eval_tc_cm*.cu
+extern template int launch_tc<2>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<4>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<8>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<12>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<16>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<18>(const EvalArgs&, int, int, cudaStream_t);
+extern template int launch_tc<24>(const EvalArgs&, int, int, cudaStream_t);
+
 namespace {
-
-constexpr int kThreads = 256;
-constexpr int kPersistentBelow = 64;  // mean primitives per tile
-constexpr int kWarps = 8;
-constexpr int kK = 8;        // K per tcgen05.mma.kind::tf32
-constexpr int kN = 32;       // class weights + sigma, padded
-constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
-constexpr uint32_t kIdesc = tc::idesc_tf32(128, kN, 1, 1);
-
-template <int CM>
-struct TcShape {
-  static_assert(CM + 1 <= kN, "sigma column must fit in N");
-  static constexpr int kLRow = (CM + 1 + 3) & ~3;
-  static constexpr int kChunk = CM <= 18 ? 120 : 104;
-  // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
-  static constexpr int kA = 0;
-  static constexpr int kB = kA + kWarps * 2 * 4096;
-  // staged primitives: record (40 words) + class weights/sigma (kLRow) each
-  static constexpr int kStride = kRecWords + kLRow;  // words
-  static constexpr int kRec = kB + kWarps * 2 * 1024;
-  // per-warp hit lists (offsets of staged primitives in 16 B units): primitives
-  // whose window covers the warp's whole block from the front, the rest from
-  // the back
-  static constexpr int kList = kRec + kChunk * kStride * 4;
-  static_assert(kStride % 4 == 0, "16-byte aligned staging");
-  static constexpr int kBm = kList + kWarps * kChunk * 2;  // staged block masks (u16)
-  static constexpr int kBar = (kBm + kChunk * 2 + 7) & ~7;
-  static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
-  static constexpr int kEnd = kMisc + 4 + kWarps * 4 + 4;  // + next-tile slot
-  // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
-  // holding z-adjacent voxels hit different banks
-  static constexpr int kStage = 16 * ((64 * CM + 8) * 4 + 72 * 4 + 72);
-  static constexpr int kBody = kEnd > kStage ? kEnd : kStage;
-  static constexpr int kSmem = kBody + 1024;               // + alignment slack
-  static_assert(kSmem <= 113 * 1024, "two CTAs per SM");
-  static_assert(kStage <= kMisc, "staging must not overwrite the flags");
-};
-
-__device__ __forceinline__ float tf32_hi(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-}
-
-template <int CM, int FIELD, bool PERSIST>
-__global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
-  using S = TcShape<CM>;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* s_rec = smem + S::kRec;
-  uint16_t* s_list = reinterpret_cast<uint16_t*>(smem + S::kList);
-  uint16_t* s_bm = reinterpret_cast<uint16_t*>(smem + S::kBm);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
-  int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
-
-  int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + kWarps * 4);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  // ---- TMEM + barriers ----
-  if (warp == 0) {
-    tc::tmem_alloc(s_tmem, kTmemCols);
-    tc::tmem_relinquish();
-  }
-  if (lane == 0) tc::mbar_init(&s_bar[warp], 1);
-  if (tid == 0) tc::fence_mbar_init();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem_base = *s_tmem;
-  const uint32_t d_tmem = tmem_base + (uint32_t)(warp * kN);
-
-  uint8_t* a_hi = smem + S::kA + warp * 8192;
-  uint8_t* a_lo = a_hi + 4096;
-  uint8_t* b_hi = smem + S::kB + warp * 2048;
-  uint8_t* b_lo = b_hi + 1024;
-  // MN-major BASE32B: A 128 rows (LBO 512, SBO 2048), B 32 rows (LBO 512, SBO 512)
-  const uint64_t da_hi = tc::smem_desc_mn32(tc::smem_u32(a_hi), 512, 2048);
-  const uint64_t da_lo = tc::smem_desc_mn32(tc::smem_u32(a_lo), 512, 2048);
-  const uint64_t db_hi = tc::smem_desc_mn32(tc::smem_u32(b_hi), 512, 512);
-  const uint64_t db_lo = tc::smem_desc_mn32(tc::smem_u32(b_lo), 512, 512);
-
-  int kk = 0;            // primitives in the open K step
-  int groups = 0;        // K steps issued by this warp
-  uint32_t phase = 0;    // parity of the next mbarrier completion to wait for
-  bool pending = false;  // an issued K step not yet known complete
-
-  auto wait_free = [&]() {
-    if (pending) {
-      tc::mbar_wait(&s_bar[warp], phase);
-      phase ^= 1u;
-      pending = false;
-    }
-  };
-
-  // primitive in K slot k: A rows lane*4 + v (one STS.128), B row lane
-  // per-lane parts of the operand offsets (tc::mn32_offset with mn = lane*4
-  // for A, mn = lane for B); the K slot adds a uniform part and a swizzle XOR
-  // The lane parts (bits 2-6, 9-10) and the K-slot parts (bits 7-8, 9 or 11)
-  // occupy disjoint bits except the swizzle bits 5-6, so offset = lane ^ slot.
-  const uint32_t a_lane = (uint32_t)((lane >> 3) * 512 + (lane & 1) * 16) |
-                          (uint32_t)(((lane >> 1) & 3) << 5);
-  const uint32_t b_lane = (uint32_t)((lane & 7) * 4) | (uint32_t)(((lane >> 3) & 3) << 5);
-  auto store_k = [&](int k, const float(&w)[kVPT], float cw) {
-    // slot part: (k & 3) * 160 | (k >> 2) << 11 (A), << 9 (B), as sums
-    const uint32_t k160 = (uint32_t)k * 160u, k4 = (uint32_t)(k & 4);
-    const uint32_t ao = a_lane ^ (k160 + k4 * 352u);
-    const uint32_t bo = b_lane ^ (k160 - k4 * 32u);
-    float4 h, l;
-    h.x = tf32_hi(w[0]);
-    h.y = tf32_hi(w[1]);
-    h.z = tf32_hi(w[2]);
-    h.w = tf32_hi(w[3]);
-    l.x = w[0] - h.x;
-    l.y = w[1] - h.y;
-    l.z = w[2] - h.z;
-    l.w = w[3] - h.w;
-    *reinterpret_cast<float4*>(a_hi + ao) = h;
-    *reinterpret_cast<float4*>(a_lo + ao) = l;
-    const float ch = tf32_hi(cw);
-    *reinterpret_cast<float*>(b_hi + bo) = ch;
-    *reinterpret_cast<float*>(b_lo + bo) = cw - ch;
-  };
-  auto issue = [&]() {
-    tc::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tc::fence_after_sync();
-      tc::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, groups > 0 ? 1u : 0u);
-      tc::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
-      tc::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, 1u);
-      tc::mma_commit(&s_bar[warp]);
-    }
-    __syncwarp();
-    ++groups;
-    pending = true;
-    kk = 0;
-  };
-  // ---- persistent loop over tiles: tile 0 of this CTA is blockIdx.x, the
-  // rest come from a global counter (dynamic balance; tiles vary from 0 to
-  // hundreds of primitives).  TMEM, barriers and descriptors are set up once;
-  // the first chunk of the next tile is staged (cp.async) while the epilogue
-  // of the current one runs when the epilogue staging leaves s_rec alone.
-  constexpr bool kPrefetch = S::kStage <= S::kRec;
-  auto stage_chunk = [&](int64_t fb, int c0, int n) {
-    // two threads per primitive, every 16-byte piece in flight at once
-    static_assert(2 * S::kChunk <= kThreads, "staging map");
-    const int j = tid >> 1;
-    if (j < n) {
-      if ((tid & 1) == 0) s_bm[j] = A.bmask[c0 + j];
-      const int64_t g = fb + A.prim_ids[c0 + j];
-      const float4* rsrc = reinterpret_cast<const float4*>(A.recs + g * kRecWords);
-      const float4* lsrc = reinterpret_cast<const float4*>(A.lrows + g * A.lrow);
-      const uint32_t dst = tc::smem_u32(s_rec + j * S::kStride * 4);
-#pragma unroll
-      for (int q = tid & 1; q < S::kStride / 4; q += 2)
-        tc::cp_async16(dst + q * 16, q < kRecWords / 4 ? rsrc + q : lsrc + (q - kRecWords / 4));
-    }
-  };
-  int tile_g = blockIdx.x;
-  bool prefetched = false;
-  while (tile_g < A.n_tiles) {
-    const int f = tile_g / A.tiles_per_frame;
-    const int t = tile_g - f * A.tiles_per_frame;
-    const int tx = t % A.ntx;
-    const int ty = (t / A.ntx) % A.nty;
-    const int tz = t / (A.ntx * A.nty);
-    const int bx0 = tx * kTileX + (warp & 1) * 4;
-    const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
-    const int bz0 = tz * kTileZ + (warp >> 2) * 8;
-    const int x = bx0 + (lane & 3);
-    const int y = by0 + ((lane >> 2) & 3);
-    const int z0 = bz0 + (lane >> 4) * 4;
-    kk = 0;
-    groups = 0;
-    // claim the next tile now; the result is only needed at the epilogue
-    const int claimed = (PERSIST && tid == 0) ? atomicAdd(A.tile_counter, 1) : 0;
-    const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
-    const int64_t fbase = (int64_t)f * A.n_prims;
-    for (int c0 = beg; c0 < end; c0 += S::kChunk) {
-      const int n = min(S::kChunk, end - c0);
-      if (!(prefetched && c0 == beg)) {
-        __syncthreads();  // every warp is done with the previous chunk
-        stage_chunk(fbase, c0, n);
-      }
-      tc::cp_async_wait_all();
-      __syncthreads();
-      uint16_t* lst = s_list + warp * S::kChunk;
-      int n_in = 0, n_part = 0;  // warp-uniform list lengths
-      const unsigned lt = (1u << lane) - 1u;
-      for (int q = 0; q * 32 < n; ++q) {
-        const int j = q * 32 + lane;
-        // this warp's bits of the precomputed block masks (block_masks_kernel)
-        const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
-        const bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
-        const unsigned mi = __ballot_sync(0xffffffffu, inside);
-        const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
-        const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
-        if (inside) lst[n_in + __popc(mi & lt)] = off;
-        if (hit && !inside) lst[S::kChunk - 1 - (n_part + __popc(mp & lt))] = off;
-        n_in += __popc(mi);
-        n_part += __popc(mp);
-      }
-      __syncwarp();
-      auto push = [&](const float(&w)[kVPT], float cw) {
-        if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
-        store_k(kk, w, cw);
-        if (++kk == kK) issue();
-      };
-      // class weight n = lane (sigma at CM), zero beyond
-      auto class_weight = [&](int off) {
-        return lane < S::kLRow ? reinterpret_cast<const float*>(s_rec + off + kRecWords * 4)[lane]
-                               : 0.0f;
-      };
-      // whole-block primitives first (no per-voxel window test), then the rest,
-      // each in ascending primitive order
-      const int n_tot = n_in + n_part;
-      auto off_at = [&](int k) {
-        return (int)(k < n_in ? lst[k] : lst[S::kChunk - 1 - (k - n_in)]) << 4;
-      };
-      if constexpr (FIELD == 6 || FIELD == 7) {
-        // two-stage software pipeline: the logs of primitive k interleave with
-        // the exps of primitive k-1 (independent chains for the latency-bound
-        // SFU/FMA mix); the hand-off lives in registers
-        auto step = [&](int k, int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
-          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-          nxt.cw = class_weight(off);
-          const bool part = k >= n_in;
-          if (wants_acc<FIELD>(R)) {
-            if (part) {
-              stage_exps<1>(cur, w);
-              stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
-            } else {
-              stage_exps<2>(cur, w);
-              stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
-            }
-          } else {
-            if (part) {
-              stage_exps<3>(cur, w);
-              stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
-            } else {
-              stage_exps<4>(cur, w);
-              stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
-            }
-          }
-        };
-        if (n_tot > 0) {
-          PairState s0, s1;
-          float w[kVPT];
-          {
-            const int off = off_at(0);
-            const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-            s0.cw = class_weight(off);
-            if (wants_acc<FIELD>(R)) {
-              if (n_in == 0)
-                stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
-              else
-                stage_logs<FIELD == 6, false, true>(R, x, y, z0, s0);
-            } else {
-              if (n_in == 0)
-                stage_logs<FIELD == 6, true, false>(R, x, y, z0, s0);
-              else
-                stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
-            }
-          }
-          // list entries are read one step ahead (past the end: harmless reads
-          // inside the CTA's shared memory, discarded)
-          int k = 1, off = off_at(1);
-          for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
-            const int off1 = off_at(k + 1);
-            step(k, off, s1, s0, w);
-            push(w, s0.cw);
-            off = off_at(k + 2);
-            step(k + 1, off1, s0, s1, w);
-            push(w, s1.cw);
-          }
-          if (k < n_tot) {
-            step(k, off, s1, s0, w);
-            push(w, s0.cw);
-            stage_exps(s1, w);
-            push(w, s1.cw);
-          } else {
-            stage_exps(s0, w);
-            push(w, s0.cw);
-          }
-        }
-      } else {
-        for (int k = 0; k < n_tot; ++k) {
-          const int off = off_at(k);
-          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-          float w[kVPT];
-          pair_weights<FIELD, true>(R, x, y, z0, w);
-          push(w, class_weight(off));
-        }
-      }
-    }
-    if (kk > 0) {  // close the last K step with zero columns
-      const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};
-      for (int k = kk; k < kK; ++k) store_k(k, zw, 0.0f);
-      issue();
-    }
-    wait_free();
-    if (lane == 0) s_has[warp] = groups > 0;
-    // next tile (one atomic per CTA), published by the barrier below
-    if (PERSIST && tid == 0) *s_next = (int)gridDim.x + claimed;
-    tc::fence_before_sync();
-    __syncthreads();  // all MMAs complete; operand smem is free for staging
-    tc::fence_after_sync();
-    const int next_tile = PERSIST ? *s_next : A.n_tiles;
-    prefetched = false;
-    if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
-      const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
-      if (ne > nb) {
-        const int nf = next_tile / A.tiles_per_frame;
-        stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
-        prefetched = true;
-      }
-    }
-
-    // ---- epilogue: TMEM -> finalize -> staged coalesced stores -------------
-    const int C = A.n_classes;
-    const int nx = A.nx, ny = A.ny, nz = A.nz;
-    const int x_t = tx * kTileX, y_t = ty * kTileY, z_t = tz * kTileZ;
-    const int zpc = 64 * C + 8;                          // padded z pitches
-    constexpr int zpo = 72;
-    float* s_vc = reinterpret_cast<float*>(smem);        // [16][zpc]
-    float* s_vo = s_vc + 16 * zpc;                       // [16][zpo]
-    uint8_t* s_lab = reinterpret_cast<uint8_t*>(s_vo + 16 * zpo);
-    const int qd = warp & 3;  // TMEM lane quarter this warp may access
-#pragma unroll 1
-    for (int i = 0; i < 4; ++i) {
-      const int mb = (warp & 4) + i;  // M block (= producing warp)
-      float vals[32];
-      if (s_has[mb]) {
-        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN), vals);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
-      }
-      // TMEM lane 32*qd + lane = row = src_lane*4 + v of block mb
-      const int src = qd * 8 + (lane >> 2), v = lane & 3;
-      const int vx = (mb & 1) * 4 + (src & 3);
-      const int vy = ((mb >> 1) & 1) * 4 + ((src >> 2) & 3);
-      const int vz = (mb >> 2) * 8 + (src >> 4) * 4 + v;
-      const int loc = vx + kTileX * vy;  // within the z layer
-      int best = 0;
-      float bv = vals[0];
-#pragma unroll
-      for (int k = 1; k < CM; ++k)
-        if (k < C && vals[k] > bv) {
-          bv = vals[k];
-          best = k;
-        }
-      const float vo = vals[CM];
-      if (A.v_c) {
-        if ((CM & 1) == 0 && C == CM) {  // 8-byte stores: zpc and loc * C are even
-          float2* d2 = reinterpret_cast<float2*>(s_vc + vz * zpc + loc * CM);
-#pragma unroll
-          for (int k = 0; k < CM / 2; ++k) d2[k] = make_float2(vals[2 * k], vals[2 * k + 1]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < CM; ++k)
-            if (k < C) s_vc[vz * zpc + loc * C + k] = vals[k];
-        }
-      }
-      s_vo[vz * zpo + loc] = vo;
-      s_lab[vz * zpo + loc] = (vo < A.tau) ? (uint8_t)A.free_label : (uint8_t)best;
-    }
-    tc::fence_proxy_async_smem();  // staging -> visible to the bulk-copy engine
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    // rows of 8 voxels: this warp owns y row y_t + warp (8 warps = the tile's
-    // 8 y rows) for every z layer, so the row base just steps by nx*ny
-    const int64_t V = (int64_t)nx * ny * nz;
-    const int xw = min(kTileX, nx - x_t);
-    const int yy = y_t + warp;
-    if (yy < ny) {
-    const int zend = min(kTileZ, nz - z_t);
-    const int64_t gv0 = (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * z_t);
-    const int64_t zstep = (int64_t)nx * ny;
-    // Full rows whose global addresses are 16-byte aligned go out as bulk
-    // async copies (one lane per z layer: the v_c row of 8*C floats and the
-    // v_o row of 8 floats) and one 8-byte label store; the rest take the
-    // lane-parallel path.  Alignment is uniform per launch (row and layer
-    // strides), so the choice is warp-uniform.
-    const bool full = xw == kTileX;
-    const bool vc_bulk = !A.v_c || (full && ((nx * C) & 3) == 0 && ((V * C) & 3) == 0 &&
-                                    (reinterpret_cast<uintptr_t>(A.v_c) & 15) == 0);
-    const bool vo_bulk = !A.v_o || (full && (nx & 3) == 0 && (V & 3) == 0 &&
-                                    (reinterpret_cast<uintptr_t>(A.v_o) & 15) == 0);
-    const bool lab8 = full && (nx & 7) == 0 && (V & 7) == 0 &&
-                      (reinterpret_cast<uintptr_t>(A.labels) & 7) == 0;
-    if (vc_bulk && vo_bulk && lab8) {
-      if (lane < zend) {
-        const int zl = lane;
-        const int64_t gv = gv0 + zl * zstep;
-        if (A.v_c)
-          tc::bulk_store(A.v_c + gv * C, tc::smem_u32(s_vc + zl * zpc + warp * kTileX * C),
-                         (uint32_t)(kTileX * C * 4));
-        if (A.v_o)
-          tc::bulk_store(A.v_o + gv, tc::smem_u32(s_vo + zl * zpo + warp * kTileX),
-                         (uint32_t)(kTileX * 4));
-        *reinterpret_cast<uint2*>(A.labels + gv) =
-            *reinterpret_cast<const uint2*>(s_lab + zl * zpo + warp * kTileX);
-      }
-      // commit + wait outside the per-lane issue (which the compiler runs as
-      // a loop over lanes): all copies are in flight before any lane waits;
-      // the staging must outlive their reads
-      __syncwarp();
-      tc::bulk_commit_wait_read();
-    } else {
-    int64_t gv = gv0;
-    const int nel = xw * C;
-    const bool vec4 = (nel & 3) == 0 && ((kTileX * C) & 3) == 0;
-    const int nel4 = nel >> 2;
-    for (int zl = 0; zl < zend; ++zl, gv += zstep) {
-      if (A.v_c) {
-        const float* src = s_vc + zl * zpc + warp * kTileX * C;  // 16-byte aligned
-        float* dst = A.v_c + gv * C;
-        if (vec4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-          const float4* s4 = reinterpret_cast<const float4*>(src);
-          float4* d4 = reinterpret_cast<float4*>(dst);
-          for (int e = lane; e < nel4; e += 32) d4[e] = s4[e];
-        } else {
-          for (int e = lane; e < nel; e += 32) dst[e] = src[e];
-        }
-      }
-      if (lane < xw) {
-        if (A.v_o) A.v_o[gv + lane] = s_vo[zl * zpo + warp * kTileX + lane];
-        A.labels[gv + lane] = s_lab[zl * zpo + warp * kTileX + lane];
-      }
-    }
-    }  // lane-parallel path
-    }  // yy < ny
-    // all TMEM reads and bulk-copy reads of the staging are done before the
-    // next tile's MMAs and operand stores reuse them
-    if (PERSIST && next_tile < A.n_tiles) {
-      tc::fence_before_sync();
-      __syncthreads();
-      tc::fence_after_sync();
-    }
-    tile_g = next_tile;
-  }  // tile loop
-  if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
-}
 
 // Per (tile, primitive) entry: which of the tile's 8 warp blocks the
 // primitive may reach (bits 0-7) and which blocks lie entirely inside its
@@ -549,41 +109,6 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
     }
   }
   bmask[e] = (uint16_t)m;
-}
-
-template <int CM>
-int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
-  using S = TcShape<CM>;
-  // never more than two CTAs per SM: each holds 256 of the 512 TMEM columns
-  constexpr int smem = S::kSmem > 80 * 1024 ? S::kSmem : 80 * 1024;
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm < 1) n_sm = 148;
-  }
-  bool persist = (field == 6 || field == 7) && A.tile_counter &&
-                 A.n_entries < (int64_t)kPersistentBelow * n_tiles && n_tiles > 2 * n_sm;
-  if (const char* pe = std::getenv("SQV_PERSIST"))  // tests / A-B: force 0 or 1
-    persist = (field == 6 || field == 7) && A.tile_counter && std::atoi(pe) != 0;
-  auto kern = field == 9   ? eval_tc_kernel<CM, 9, false>
-              : field == 8 ? eval_tc_kernel<CM, 8, false>
-              : field == 6 ? (persist ? eval_tc_kernel<CM, 6, true> : eval_tc_kernel<CM, 6, false>)
-                           : (persist ? eval_tc_kernel<CM, 7, true> : eval_tc_kernel<CM, 7, false>);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-      cudaSuccess)
-    return check_launch("eval_tc_kernel attribute");
-  // Sparse tiles (few primitives each: per-tile setup, staging latency and
-  // epilogue dominate) run persistent — two CTAs per SM, tiles handed out by
-  // A.tile_counter, the next tile's first chunk staged under the epilogue.
-  // Dense tiles run one CTA per tile (measured faster there).
-  const EvalArgs& B = A;
-  const int grid = persist ? 2 * n_sm : n_tiles;
-  if (grid < 1) return SQV_OK;
-  kern<<<grid, kThreads, smem, s>>>(B);
-  count_launch();
-  return check_launch("eval_tc_kernel");
 }
 
 }  // namespace
