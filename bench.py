@@ -336,7 +336,7 @@ def run_ours(a, rank, world, local_rank):
                 "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": traffic,
                 "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": B * spec.n_voxels * (1 + 4 + 4 * C),
-                "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc.cu)" if os.environ.get(
+                "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc_impl.cuh)" if os.environ.get(
                     "SQV_EVAL") != "ffma" else "eval_kernel (FFMA, sqv_eval.cu)",
                 "algorithmic": f"{MUFU_PER_PAIR} MUFU per in-window (primitive, voxel) pair x "
                                f"{pairs_per_launch:.4e} pairs per launch",
