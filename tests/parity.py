@@ -3,9 +3,12 @@
 * bins, windows, pair counts and confusion counts: bit-exact;
 * densities:
     precision="strict" (default):
-    |v_o - ref| <= 1e-5 * max(ref, 1e-3*tau)   1e-5 relative down to 1e-3*tau;
+    |v_o - ref| <= 1e-5 * max(ref, floor)      1e-5 relative down to the floor,
+    floor = max(1e-3*tau, 1e-5)                1e-3*tau, never
+                                               below the default tau's 1e-5
+                                               (tau = 0 has no tau scale);
     precision="fast":
-    |v_o - ref| <= 2e-5 * max(ref, 1e-3*tau)   (the SFU log2 error, 2^-22
+    |v_o - ref| <= 2e-5 * max(ref, floor)      (the SFU log2 error, 2^-22
                                                absolute, is amplified by
                                                2/eps1 <= 10 in F and by F in
                                                exp(-F); z steps are rounded once);
@@ -20,6 +23,7 @@ import numpy as np
 VO_REL = 1e-5                # strict
 VO_REL_TAIL = 2e-5           # fast
 VO_TAIL_FLOOR_FRAC_TAU = 1e-3
+VO_MIN_FLOOR = 1e-5          # = 1e-3 * the default tau (0.01)
 LABEL_GAP = 1e-5
 MIN_AGREEMENT = 0.9999
 
@@ -30,7 +34,7 @@ def vo_check(gpu, ref, tau, mode="strict"):
     err = np.abs(gpu - ref)
     out = {}
     bad = np.zeros(err.shape, bool)
-    tail_floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, 1e-9)
+    tail_floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
     tiers = ((("tier1", VO_REL, tail_floor),) if mode == "strict" else
              (("tier1", VO_REL_TAIL, tail_floor),))
     for name, rel, floor in tiers:

@@ -404,3 +404,48 @@ def test_persistent_and_per_tile_evaluators_bit_identical(monkeypatch, n_prims):
             outs.append({k: getattr(r, k).cpu().numpy() for k in ("labels", "v_o", "v_c")})
         for k in ("labels", "v_o", "v_c"):
             np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=f"{prec} {k}")
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_randomized_configurations(case):
+    """Sampled grid shapes (tile-ragged dims, offset origins, fine/coarse
+    resolutions), class counts 1..24, both semantic modes, both precisions,
+    truncated or not, ragged n_valid, persistent or per-tile evaluator:
+    bins exact, densities and labels at the mode's tolerance."""
+    P = _pkg()
+    import os
+    from paper_2511_17361_b200.core import PrimitiveBatch
+    rng = np.random.default_rng(1000 + case)
+    dims = (int(rng.integers(5, 45)), int(rng.integers(5, 45)), int(rng.integers(3, 36)))
+    res = float(rng.choice([0.2, 0.37, 0.5]))
+    origin = tuple(float(x) for x in rng.uniform(-6, 2, 3))
+    C = int(rng.choice([1, 2, 5, 12, 17, 18, 19, 23, 24]))
+    mode = "prob-sum" if rng.random() < 0.4 else "logit-sum"
+    prec = "fast" if rng.random() < 0.3 else "strict"
+    truncate = rng.random() < 0.75
+    F, N = int(rng.integers(1, 4)), int(rng.integers(1, 60))
+    hi = tuple(o + d * res for o, d in zip(origin, dims))
+    spec = P.VoxelGridSpec(origin, dims, res)
+    cfg = P.VoxelizeConfig(tau=float(rng.choice([0.0, 0.01, 0.2])),
+                           neighborhood_radius=int(rng.integers(0, 6)), semantic_mode=mode,
+                           precision=prec)
+    b = _scene(77 + case, N, C, frames=F, origin=origin, dims=dims, resolution=res,
+               smax=float(rng.choice([1.0, 4.0])))
+    nv = rng.integers(0, N + 1, F).astype(np.int32)
+    b = PrimitiveBatch(b.mu, b.scale, b.rot, b.opacity, b.eps, b.logits, n_valid=nv)
+    os.environ["SQV_PERSIST"] = str(case % 2)
+    try:
+        out = _run(b, spec, cfg, C, truncate=truncate, bins=True)
+    finally:
+        del os.environ["SQV_PERSIST"]
+    ref, grid = _oracle(b, spec, cfg, out["free_code"], truncate=truncate)
+    np.testing.assert_array_equal(out["windows"], ref["windows"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert out["n_pairs"] == ref["n_pairs"]
+    vo = vo_check(out["v_o"], ref["v_o"], cfg.tau, prec)
+    assert vo["n_bad"] == 0, vo
+    lab = label_check(out["labels"], ref["labels"], ref["v_o"], ref["v_c"], cfg.tau,
+                      out["free_code"])
+    assert lab["n_unexplained"] == 0, lab  # tiny grids: no agreement-rate floor
