@@ -132,17 +132,23 @@ float tau_f32(double tau) {
 // Opt-in stage profiler (sqv_profile_*): CUDA events on the caller's stream.
 // The previous call's emit/sort/eval events are folded in at the next
 // call's header readback (stream order guarantees they completed).
+// Stage timer: a ring of event sets, one per sqv_voxelize call, so calls on
+// different streams (pipelined batches) never overwrite each other's events;
+// a set is folded once its last event has completed (or at read time).
 struct Profiler {
+  static constexpr int kRing = 8;
   std::mutex mu;
   bool on = false;
-  bool pending = false;
   bool created = false;
-  cudaEvent_t ev[5];
+  cudaEvent_t ev[kRing][5];
+  bool pending[kRing] = {};
+  int next = 0;
   double ms[SQV_NSTAGES] = {0, 0, 0, 0};
   long long calls = 0;
   void ensure() {
     if (!created) {
-      for (auto& e : ev) cudaEventCreate(&e);
+      for (auto& set : ev)
+        for (auto& e : set) cudaEventCreate(&e);
       created = true;
     }
   }
@@ -151,13 +157,37 @@ struct Profiler {
     cudaEventElapsedTime(&m, a, b);
     return m;
   }
-  void fold_pending() {
-    if (!pending) return;
-    const double m1 = el(ev[2], ev[3]), m2 = el(ev[3], ev[4]);
+  void fold(int i) {
+    const double m0 = el(ev[i][0], ev[i][1]), m1 = el(ev[i][2], ev[i][3]),
+                 m2 = el(ev[i][3], ev[i][4]);
+    ms[0] += m0;
     ms[1] += m1;
     ms[2] += m2;
-    ms[3] += m1 + m2;
-    pending = false;
+    ms[3] += m0 + m1 + m2;
+    calls++;
+    pending[i] = false;
+  }
+  void fold_ready() {
+    for (int i = 0; i < kRing; ++i)
+      if (pending[i] && cudaEventQuery(ev[i][4]) == cudaSuccess) fold(i);
+  }
+  void fold_all() {
+    for (int i = 0; i < kRing; ++i)
+      if (pending[i]) {
+        cudaEventSynchronize(ev[i][4]);
+        fold(i);
+      }
+  }
+  int acquire() {  // caller holds mu
+    ensure();
+    fold_ready();
+    const int i = next;
+    next = (next + 1) % kRing;
+    if (pending[i]) {  // more than kRing calls in flight: wait for the oldest
+      cudaEventSynchronize(ev[i][4]);
+      fold(i);
+    }
+    return i;
   }
 };
 Profiler g_prof;
@@ -245,10 +275,11 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   if (!hmap) return set_error(SQV_ERR_CUDA, "mapped header allocation failed");
 
   const bool prof = g_prof.on;
+  int pset = 0;
   if (prof) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
-    g_prof.ensure();
-    cudaEventRecord(g_prof.ev[0], s);
+    pset = g_prof.acquire();
+    cudaEventRecord(g_prof.ev[pset][0], s);
   }
   // K1 prep
   if (FN > 0) {
@@ -279,7 +310,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   }
   // K2 scan of per-primitive tile counts -> entry offsets, total -> header
   if (int rc = scan_exclusive(counts, offs, FN, scan_tmp, &hdr->n_entries, s)) return rc;
-  if (prof) cudaEventRecord(g_prof.ev[1], s);
+  if (prof) cudaEventRecord(g_prof.ev[pset][1], s);
   header_out_kernel<<<1, 1, 0, s>>>(hdr, hmap);
   count_launch();
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("header readback");
@@ -288,14 +319,6 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     const volatile long long* m = reinterpret_cast<const volatile long long*>(hmap);
     long long* d = reinterpret_cast<long long*>(&h);
     for (int k = 0; k < 4; ++k) d[k] = m[k];
-  }
-  if (prof) {
-    std::lock_guard<std::mutex> lk(g_prof.mu);
-    g_prof.fold_pending();
-    const double m0 = Profiler::el(g_prof.ev[0], g_prof.ev[1]);
-    g_prof.ms[0] += m0;
-    g_prof.ms[3] += m0;
-    g_prof.calls++;
   }
   if (h.bad_word != ~0ULL) {
     if (bad_prim) *bad_prim = (int64_t)(h.bad_word >> 8);
@@ -315,7 +338,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   int* vals_b = (int*)(ws + L.vals_b);
   int* radix_tmp = (int*)(ws + L.radix_tmp);
 
-  if (prof) cudaEventRecord(g_prof.ev[2], s);
+  if (prof) cudaEventRecord(g_prof.ev[pset][2], s);
   // K3 emit + K4 radix sort + tile offsets
   int which = 0;
   if (E > 0) {
@@ -372,7 +395,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.n_tiles = (int)FT;
   A.tile_counter = reinterpret_cast<int*>(&hdr->pad);  // zeroed with the header
   A.n_entries = E;
-  if (prof) cudaEventRecord(g_prof.ev[3], s);
+  if (prof) cudaEventRecord(g_prof.ev[pset][3], s);
   {
     // tcgen05 evaluator by default; SQV_EVAL=ffma selects the CUDA-core one (A/B runs)
     const char* ev = std::getenv("SQV_EVAL");
@@ -386,8 +409,9 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
       return rc;
   }
   if (prof) {
-    cudaEventRecord(g_prof.ev[4], s);
-    g_prof.pending = true;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    cudaEventRecord(g_prof.ev[pset][4], s);
+    g_prof.pending[pset] = true;
   }
 
   if (bins) {
@@ -518,9 +542,8 @@ int sqv_profile_enable(int on) {
 
 int sqv_profile_read(double* ms, int64_t* calls, int reset) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
-  if (g_prof.pending) {
-    cudaEventSynchronize(g_prof.ev[4]);
-    g_prof.fold_pending();
+  {
+    g_prof.fold_all();
   }
   if (ms)
     for (int k = 0; k < SQV_NSTAGES; ++k) ms[k] = g_prof.ms[k];

@@ -172,7 +172,7 @@ class Voxelizer:
         c.window_extent = float(cfg.window_extent)
         c.precision = PRECISIONS.index(cfg.precision)
         self._cfg = c
-        self._ws = None
+        self._ws = [None, None]  # one workspace per pipelined stream slot
         self.tiles_per_frame = int(self.L.sqv_tiles_per_frame(ctypes.byref(self._grid)))
 
     # ---- inputs -----------------------------------------------------------
@@ -189,11 +189,37 @@ class Voxelizer:
         nv = None if batch.n_valid is None else self._dev(batch.n_valid, t.int32)
         return PrimitiveBatch(*f, n_valid=nv)
 
-    def _workspace(self, nbytes: int):
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = self.torch.empty(int(nbytes * 1.25) + 4096, dtype=self.torch.uint8,
-                                        device=self.device)
-        return self._ws
+    def _workspace(self, nbytes: int, slot: int = 0):
+        ws = self._ws[slot]
+        if ws is None or ws.numel() < nbytes:
+            # allocated on the stream that will use it (torch's allocator
+            # keys blocks by stream)
+            ws = self.torch.empty(int(nbytes * 1.25) + 4096, dtype=self.torch.uint8,
+                                  device=self.device)
+            self._ws[slot] = ws
+        return ws
+
+    def run_many(self, batches, outs, *, dense: bool = True, on_device=None):
+        """Voxelize device-resident batches back to back on two alternating
+        CUDA streams, so the per-batch binning (prep, the one header
+        readback, emit, sort, masks) of batch k+1 overlaps the evaluation of
+        batch k.  ``outs`` = two preallocated results (``alloc``), reused
+        alternately; ``on_device(k, result)`` runs on batch k's stream right
+        after it (e.g. confusion counts).  The caller's current stream waits
+        for both streams on return (no host sync)."""
+        t = self.torch
+        cur = t.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = t.cuda.Stream(self.device)
+        streams = (cur, self._side)
+        self._side.wait_stream(cur)
+        for k, b in enumerate(batches):
+            slot = k & 1
+            with t.cuda.stream(streams[slot]):
+                r = self(b, dense=dense, out=outs[slot], _slot=slot)
+                if on_device is not None:
+                    on_device(k, r)
+        cur.wait_stream(self._side)
 
     # ---- pipelined host streams ----------------------------------------------
     def stream(self, batches, *, dense: bool = True, on_device=None, labels_out=None):
@@ -272,7 +298,7 @@ class Voxelizer:
         return out
 
     def __call__(self, batch: PrimitiveBatch, *, dense: bool = True, bins: bool = False,
-                 out: VoxelizeResult | None = None) -> VoxelizeResult:
+                 out: VoxelizeResult | None = None, _slot: int = 0) -> VoxelizeResult:
         """Voxelize F frames.  Host inputs are copied to the device first
         (non_blocking from pinned memory).  ``out`` may be preallocated with
         ``alloc``; ``dense=False`` keeps v_o/v_c on chip (labels only)."""
@@ -281,7 +307,7 @@ class Voxelizer:
             raise ValueError(f"batch has {batch.n_classes} classes, voxelizer expects {self.C}")
         with t.cuda.device(self.device):
             try:
-                return self._run(batch, dense, bins, out)
+                return self._run(batch, dense, bins, out, _slot)
             except _lib.SqvError as e:
                 # index spaces are 32-bit per call: halve the frames and retry
                 if "split frames" not in str(e) or batch.n_frames < 2 or bins:
@@ -292,14 +318,14 @@ class Voxelizer:
             part = lambda a, lo, hi: None if a is None else a[lo:hi]
             rs = [self(batch.frames(lo, hi), dense=dense,
                        out=VoxelizeResult(out.labels[lo:hi], part(out.v_o, lo, hi),
-                                          part(out.v_c, lo, hi)))
+                                          part(out.v_c, lo, hi)), _slot=_slot)
                   for lo, hi in ((0, h), (h, F))]
             out.free_code = self.free_code
             out.n_pairs = sum(r.n_pairs for r in rs)
             out.n_entries = sum(r.n_entries for r in rs)
             return out
 
-    def _run(self, batch, dense, bins, out):
+    def _run(self, batch, dense, bins, out, slot=0):
         t = self.torch
         db = self.to_device(batch)
         F, N = db.n_frames, db.n_prims
@@ -330,7 +356,7 @@ class Voxelizer:
         bad_bits = ctypes.c_int32(0)
         ws_bytes = int(self.L.sqv_workspace_bytes(F, N, self.C, ctypes.byref(self._grid), 0))
         for _attempt in range(4):
-            ws = self._workspace(ws_bytes)
+            ws = self._workspace(ws_bytes, slot)
             if bins:
                 B.prim_ids = bins_t["prim_ids"].data_ptr()
                 B.capacity = bins_t["prim_ids"].numel()
