@@ -449,3 +449,25 @@ def test_randomized_configurations(case):
     lab = label_check(out["labels"], ref["labels"], ref["v_o"], ref["v_c"], cfg.tau,
                       out["free_code"])
     assert lab["n_unexplained"] == 0, lab  # tiny grids: no agreement-rate floor
+
+
+def test_run_many_two_stream_pipeline_matches_direct_calls():
+    """Voxelizer.run_many (alternating streams, two workspaces and output
+    slots) gives the same bits as one call per batch."""
+    P = _pkg()
+    import torch
+    from paper_2511_17361_b200.scenegen import gen_frames
+    spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig()
+    vox = P.Voxelizer(spec, cfg, 18)
+    batches = [vox.to_device(gen_frames(50 + k, 2, 300 + 200 * k)) for k in range(4)]
+    direct = [vox(b, dense=True) for b in batches]
+    want = [(r.labels.cpu().numpy(), r.v_c.cpu().numpy()) for r in direct]
+    outs = [vox.alloc(2), vox.alloc(2)]
+    got = []
+    vox.run_many(batches, outs, on_device=lambda k, r: got.append(
+        (r.labels.clone(), r.v_c.clone())))
+    torch.cuda.synchronize()
+    assert len(got) == 4
+    for (gl, gc), (wl, wc) in zip(got, want):
+        np.testing.assert_array_equal(gl.cpu().numpy(), wl)
+        np.testing.assert_array_equal(gc.cpu().numpy(), wc)
