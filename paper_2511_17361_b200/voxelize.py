@@ -226,13 +226,20 @@ class Voxelizer:
         """Voxelize a sequence of host batches (pinned torch tensors for real
         overlap) with copies overlapped: the H2D copy of batch k+1 and the D2H
         copy of batch k-1's labels run on two copy streams while batch k is
-        evaluated on the current stream.  ``on_device(k, result)`` is called
-        on the compute stream right after batch k (e.g. confusion counts).
+        evaluated; consecutive batches alternate two compute streams (the
+        current one and a side stream, as in ``run_many``) so a batch's
+        binning overlaps the previous evaluation.  ``on_device(k, result)`` is
+        called on batch k's compute stream right after it (e.g. confusion
+        counts).
         Returns the host label tensors [F, nz, ny, nx] (uint8, pinned), valid
         when this call returns."""
         t = self.torch
         nx, ny, nz = self.spec.dims
-        comp = t.cuda.current_stream(self.device)
+        comp0 = t.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = t.cuda.Stream(self.device)
+        comps = (comp0, self._side)
+        self._side.wait_stream(comp0)
         h2d, d2h = t.cuda.Stream(self.device), t.cuda.Stream(self.device)
         nb = len(batches)
         if nb == 0:
@@ -267,23 +274,27 @@ class Voxelizer:
             s = k & 1
             if k + 1 < nb:
                 load(k + 1)
-            comp.wait_event(ev_h2d[s])
-            if ev_out_free[s] is not None:
-                comp.wait_event(ev_out_free[s])
-            nv = batches[k].n_valid
-            db = PrimitiveBatch(*(slots[s][f] for f in PrimitiveBatch.FIELDS),
-                                n_valid=None if nv is None else self._dev(nv, t.int32))
-            res = self(db, dense=dense, out=outs[s])
-            if on_device is not None:
-                on_device(k, res)
-            done = comp.record_event()
+            comp = comps[s]
+            with t.cuda.stream(comp):
+                comp.wait_event(ev_h2d[s])
+                if ev_out_free[s] is not None:
+                    comp.wait_event(ev_out_free[s])
+                nv = batches[k].n_valid
+                db = PrimitiveBatch(*(slots[s][f] for f in PrimitiveBatch.FIELDS),
+                                    n_valid=None if nv is None else self._dev(nv, t.int32))
+                res = self(db, dense=dense, out=outs[s], _slot=s)
+                if on_device is not None:
+                    on_device(k, res)
+                done = comp.record_event()
             ev_in_free[s] = done
             with t.cuda.stream(d2h):
                 d2h.wait_event(done)
                 labels_out[k].copy_(outs[s].labels, non_blocking=True)
                 ev_out_free[s] = d2h.record_event()
         d2h.synchronize()
-        comp.synchronize()
+        comps[1].synchronize()
+        comp0.wait_stream(comps[1])
+        comp0.synchronize()
         return labels_out
 
     # ---- run ----------------------------------------------------------------
