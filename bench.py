@@ -349,11 +349,11 @@ def run_ours(a, rank, world, local_rank):
                 "eval_ms_per_launch": eval_s * 1e3,
                 "eval_share_of_step": prof["eval_ms"] / max(1e-9, dt * 1e3),
                 "stage_ms_per_step": {k: v / max(prof["calls"], 1) for k, v in prof.items()
-                                      if k in ("prep_scan_ms", "eval_ms")},
-                "stage_note": "CUDA-event spans of one step on its stream; consecutive steps "
-                              "alternate two streams (binning of k+1 under the evaluation of "
-                              "k), so the emit/sort span is not reported (it contains the "
-                              "other stream's evaluation)",
+                                      if k == "eval_ms"},
+                "stage_note": "CUDA-event span of one step's evaluation on its stream; "
+                              "consecutive steps alternate two streams (binning of k+1 under "
+                              "the evaluation of k), so the binning spans are not reported "
+                              "(they contain the other stream's evaluation)",
                 "peak_source": "sqv_microbench(MUFU) measured live on this GPU",
                 "bound_note": "the field (powers, exps) is transcendental: the SFU pipe bounds "
                               "the evaluator; the contract's hbm and tensor rooflines of the "
