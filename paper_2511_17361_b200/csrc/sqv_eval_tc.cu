@@ -65,9 +65,10 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
 #pragma unroll
   for (int q = 0; q < kRecWords / 4; ++q) dst[q] = __ldg(src + q);
   const int x0 = tx * kTileX, y0 = ty * kTileY, z0 = tz * kTileZ;
-  float ex[3], ey[3], ez[3], c0[3], h[3];
+  float ex[3], ey[3], ez[3], c0[3], h[3], stepx[3], stepy[3], stepz[3];
   const float kx = (float)x0 + 1.5f - R.cx, ky = (float)y0 + 1.5f - R.cy,
               kz = (float)z0 + 3.5f - R.cz;
+  float span = 0.0f;  // bounds |c| + h of every block: one FP32 error margin per entry
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     ex[r] = R.HL[3 * r].x + R.HL[3 * r].y;
@@ -75,38 +76,48 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
     ez[r] = R.HL[3 * r + 2].x + R.HL[3 * r + 2].y;
     c0[r] = fmaf(kz, ez[r], fmaf(ky, ey[r], fmaf(kx, ex[r], R.G[r].x + R.G[r].y)));
     h[r] = 1.5f * fabsf(ex[r]) + 1.5f * fabsf(ey[r]) + 3.5f * fabsf(ez[r]);
+    stepx[r] = 4.0f * ex[r];
+    stepy[r] = 4.0f * ey[r];
+    stepz[r] = 8.0f * ez[r];
+    span += fabsf(c0[r]) + fabsf(stepx[r]) + fabsf(stepy[r]) + fabsf(stepz[r]) + h[r];
   }
+  const float eps = 1e-4f * span;  // FP32 error of c, h (incl. the stepped centres)
+  const float cut = R.mcut + eps;
+  // window overlap / containment of the two block positions on each axis
+  const int* lo = R.lo;
+  const int* hi = R.hi;
+  const bool wx[2] = {x0 + 3 >= lo[0] && x0 <= hi[0], x0 + 7 >= lo[0] && x0 + 4 <= hi[0]};
+  const bool wy[2] = {y0 + 3 >= lo[1] && y0 <= hi[1], y0 + 7 >= lo[1] && y0 + 4 <= hi[1]};
+  const bool wz[2] = {z0 + 7 >= lo[2] && z0 <= hi[2], z0 + 15 >= lo[2] && z0 + 8 <= hi[2]};
+  const bool ix[2] = {x0 >= lo[0] && x0 + 3 <= hi[0], x0 + 4 >= lo[0] && x0 + 7 <= hi[0]};
+  const bool iy[2] = {y0 >= lo[1] && y0 + 3 <= hi[1], y0 + 4 >= lo[1] && y0 + 7 <= hi[1]};
+  const bool iz[2] = {z0 >= lo[2] && z0 + 7 <= hi[2], z0 + 8 >= lo[2] && z0 + 15 <= hi[2]};
   // sure-hit radius: (2^b + 1) M^c <= 0.5 kFCut  <=>  M <= (0.5 kFCut / (2^b + 1))^(1/c)
   const float inv_c = 1.0f / R.c;
   const float sure = ex2(inv_c * lg2(0.5f * kFCut / (ex2(R.b) + 1.0f)));
   unsigned m = 0;
 #pragma unroll
   for (int bb = 0; bb < kWarps; ++bb) {
-    const int dx = (bb & 1) * 4, dy = ((bb >> 1) & 1) * 4, dz = (bb >> 2) * 8;
-    const int bx0 = x0 + dx, by0 = y0 + dy, bz0 = z0 + dz;
-    if (bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
-        bz0 + 7 < R.lo[2] || bz0 > R.hi[2])
-      continue;
-    float mm[3], dmax = -1.0f, slack = 0.0f;
+    const int ox = bb & 1, oy = (bb >> 1) & 1, oz = bb >> 2;
+    if (!(wx[ox] && wy[oy] && wz[oz])) continue;
+    float mm[3], dmax = -1.0f;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      const float c = c0[r] + ((float)dx * ex[r] + (float)dy * ey[r] + (float)dz * ez[r]);
+      float c = c0[r];
+      if (ox) c += stepx[r];
+      if (oy) c += stepy[r];
+      if (oz) c += stepz[r];
       mm[r] = fabsf(c) - h[r];
       dmax = fmaxf(dmax, mm[r]);
-      slack += fabsf(c) + h[r];
     }
-    const float eps = 1e-4f * slack;  // FP32 error of c, h (incl. the stepped centres)
-    if (dmax > R.mcut + eps) continue;
+    if (dmax > cut) continue;
     bool hit = dmax <= sure;
     if (!hit) {
       const float F = field_F(fmaxf(mm[0] - eps, 0.0f), fmaxf(mm[1] - eps, 0.0f),
                               fmaxf(mm[2] - eps, 0.0f), R.a, R.b, R.c);
       hit = F < 1.02f * kFCut;
     }
-    if (hit) {
-      m |= 1u << bb;
-      if (block_inside(R, bx0, by0, bz0)) m |= 1u << (8 + bb);
-    }
+    if (hit) m |= (1u << bb) | ((unsigned)(ix[ox] && iy[oy] && iz[oz]) << (8 + bb));
   }
   bmask[e] = (uint16_t)m;
 }
