@@ -23,9 +23,14 @@ def main(path):
         tot[k] += float(r[iV].replace(",", ""))
         cnt[k] += 1
     T = sum(tot.values())
-    print(f"{'kernel':46s} {'launches':>8s} {'total us':>11s} {'share':>7s}")
+    # the bench's roofline denominators (mb_*: live SFU/FFMA peak
+    # microbenchmarks) run once outside the timed steps: shares of the step
+    # are over the remaining kernels
+    Ts = sum(v for k, v in tot.items() if not k.startswith("mb_"))
+    print(f"{'kernel':46s} {'launches':>8s} {'total us':>11s} {'share':>7s} {'of step':>8s}")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        print(f"{k:46s} {cnt[k]:8d} {v / 1e3:11.1f} {100 * v / T:6.1f}%")
+        step = "" if k.startswith("mb_") else f"{100 * v / Ts:7.1f}%"
+        print(f"{k:46s} {cnt[k]:8d} {v / 1e3:11.1f} {100 * v / T:6.1f}% {step:>8s}")
 
 
 if __name__ == "__main__":
