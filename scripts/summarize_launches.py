@@ -6,7 +6,7 @@ import sys
 
 
 def short(name):
-    name = name.replace("void ", "").replace("(anonymous namespace)::", "")
+    name = name.replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
     name = re.sub(r"\(.*\)$", "", name)
     return name.replace("sqv::", "")
 
