@@ -213,6 +213,32 @@ def test_fine_grid_config4_slice():
     assert_parity(out, ref, cfg.tau, out["free_code"])
 
 
+@pytest.mark.parametrize("which", ["config3", "config4"])
+def test_full_frame_configs_3_and_4(which):
+    """One full frame of config 3 (4k SQs, eps in [0.1, 2]: near-cuboids and
+    needles, clamped per core.py:162-165) and of config 4 (8k SQs on
+    400x400x32 @0.2 m, ~1.8 G pairs): bins, pair count, densities and labels
+    against the FP64 oracle at the BASELINE sizes."""
+    P = _pkg()
+    if which == "config3":
+        spec = P.VoxelGridSpec()
+        b = _scene(21, 4000, emin=0.1)
+    else:
+        spec = P.VoxelGridSpec((-40.0, -40.0, -1.0), (400, 400, 32), 0.2)
+        b = _scene(22, 8000, origin=spec.origin, dims=spec.dims, resolution=spec.resolution)
+    cfg = P.VoxelizeConfig()
+    out = _run(b, spec, cfg, 18, bins=True)
+    ref, grid = _oracle(b, spec, cfg, out["free_code"])
+    np.testing.assert_array_equal(out["windows"], ref["windows"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert out["n_pairs"] == ref["n_pairs"]
+    vo, lab = assert_parity(out, ref, cfg.tau, out["free_code"])
+    print(which, "pairs", ref["n_pairs"], "worst v_o rel", vo["worst_rel"], "agreement",
+          lab["agreement"])
+
+
 # ---- drop-in API ----------------------------------------------------------------
 
 def test_dropin_scene_api_and_spec_examples():
