@@ -432,7 +432,7 @@ def test_persistent_and_per_tile_evaluators_bit_identical(monkeypatch, n_prims):
             np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=f"{prec} {k}")
 
 
-@pytest.mark.parametrize("case", range(40))
+@pytest.mark.parametrize("case", range(int(os.environ.get("SQV_RANDOM_CASES", "40"))))
 def test_randomized_configurations(case):
     """Sampled grid shapes (tile-ragged dims, offset origins, fine/coarse
     resolutions), class counts 1..24, both semantic modes, both precisions,
