@@ -40,7 +40,8 @@ struct TcShape {
   static constexpr int kList = kRec + kChunk * kStride * 4;
   static_assert(kStride % 4 == 0, "16-byte aligned staging");
   static constexpr int kBm = kList + kWarps * kChunk * 2;  // staged block masks (u16)
-  static constexpr int kBar = (kBm + kChunk * 2 + 7) & ~7;
+  static constexpr int kAcc = kBm + kChunk * 2;  // strict: per-warp u8 lists of accurate-log primitives
+  static constexpr int kBar = (kAcc + kWarps * kChunk + 7) & ~7;
   static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
   static constexpr int kEnd = kMisc + 4 + kWarps * 4 + 4;  // + next-tile slot
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint8_t* s_rec = smem + S::kRec;
   uint16_t* s_list = reinterpret_cast<uint16_t*>(smem + S::kList);
   uint16_t* s_bm = reinterpret_cast<uint16_t*>(smem + S::kBm);
+  uint8_t* s_acc = smem + S::kAcc;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   // the first chunk of the next tile is staged (cp.async) while the epilogue
   // of the current one runs when the epilogue staging leaves s_rec alone.
   constexpr bool kPrefetch = S::kStage <= S::kRec;
+  constexpr bool kSplitAcc = FIELD == 6;
   auto stage_chunk = [&](int64_t fb, int c0, int n) {
     // two threads per primitive, every 16-byte piece in flight at once
     static_assert(2 * S::kChunk <= kThreads, "staging map");
@@ -200,13 +203,23 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
       tc::cp_async_wait_all();
       __syncthreads();
       uint16_t* lst = s_list + warp * S::kChunk;
-      int n_in = 0, n_part = 0;  // warp-uniform list lengths
+      uint8_t* lst_acc = s_acc + warp * S::kChunk;
+      int n_in = 0, n_part = 0, n_acc = 0;  // warp-uniform list lengths
       const unsigned lt = (1u << lane) - 1u;
       for (int q = 0; q * 32 < n; ++q) {
         const int j = q * 32 + lane;
         // this warp's bits of the precomputed block masks (block_masks_kernel)
         const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
-        const bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
+        bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
+        if (kSplitAcc) {  // strict: accurate-log primitives get their own list
+          const bool acc =
+              hit && reinterpret_cast<const PrimRec*>(s_rec + j * S::kStride * 4)->c > SQV_ACC_C;
+          const unsigned ma = __ballot_sync(0xffffffffu, acc);
+          if (acc) lst_acc[n_acc + __popc(ma & lt)] = (uint8_t)j;
+          n_acc += __popc(ma);
+          hit &= !acc;
+          inside &= !acc;
+        }
         const unsigned mi = __ballot_sync(0xffffffffu, inside);
         const unsigned mp = __ballot_sync(0xffffffffu, hit && !inside);
         const uint16_t off = (uint16_t)(j * (S::kStride / 4));  // 16-byte units
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
           nxt.cw = class_weight(off);
           const bool part = k >= n_in;
-          if (wants_acc<FIELD>(R)) {
+          if (!kSplitAcc && wants_acc<FIELD>(R)) {
             if (part) {
               stage_exps<1>(cur, w);
               stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
@@ -265,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             const int off = off_at(0);
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             s0.cw = class_weight(off);
-            if (wants_acc<FIELD>(R)) {
+            if (!kSplitAcc && wants_acc<FIELD>(R)) {
               if (n_in == 0)
                 stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
               else
@@ -297,6 +310,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             stage_exps(s0, w);
             push(w, s0.cw);
           }
+        }
+        // strict: the accurate-log primitives after the rest, unpipelined
+        // (their long FMA-pipe logs no longer double the pipelined loop's code)
+        for (int k = 0; k < n_acc; ++k) {
+          const int off = (int)lst_acc[k] * S::kStride * 4;
+          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+          float w[kVPT];
+          pair_weights<FIELD, true>(R, x, y, z0, w);
+          push(w, class_weight(off));
         }
       } else {
         for (int k = 0; k < n_tot; ++k) {
