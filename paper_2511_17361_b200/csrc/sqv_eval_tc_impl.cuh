@@ -249,60 +249,48 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         // two-stage software pipeline: the logs of primitive k interleave with
         // the exps of primitive k-1 (independent chains for the latency-bound
         // SFU/FMA mix); the hand-off lives in registers
-        auto step = [&](int k, int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
-          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-          nxt.cw = class_weight(off);
-          const bool part = k >= n_in;
-          if (!kSplitAcc && wants_acc<FIELD>(R)) {
-            if (part) {
+        // One pipelined pass over a list (whole-block primitives, LIVE =
+        // false, or partial ones, LIVE = true): no per-primitive branch on
+        // the list kind.  Strict mode has already moved its accurate-log
+        // primitives to lst_acc; fast mode has none.
+        auto run = [&](auto live, int cnt, auto off_of) {
+          constexpr bool LIVE = decltype(live)::value;
+          if (cnt <= 0) return;
+          auto step = [&](int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
+            const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+            nxt.cw = class_weight(off);
+            if (!kSplitAcc && wants_acc<FIELD>(R)) {
               stage_exps<1>(cur, w);
-              stage_logs<FIELD == 6, true, true>(R, x, y, z0, nxt);
+              stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, nxt);
             } else {
               stage_exps<2>(cur, w);
-              stage_logs<FIELD == 6, false, true>(R, x, y, z0, nxt);
+              stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
             }
-          } else {
-            if (part) {
-              stage_exps<3>(cur, w);
-              stage_logs<FIELD == 6, true, false>(R, x, y, z0, nxt);
-            } else {
-              stage_exps<4>(cur, w);
-              stage_logs<FIELD == 6, false, false>(R, x, y, z0, nxt);
-            }
-          }
-        };
-        if (n_tot > 0) {
+          };
           PairState s0, s1;
           float w[kVPT];
           {
-            const int off = off_at(0);
+            const int off = off_of(0);
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             s0.cw = class_weight(off);
-            if (!kSplitAcc && wants_acc<FIELD>(R)) {
-              if (n_in == 0)
-                stage_logs<FIELD == 6, true, true>(R, x, y, z0, s0);
-              else
-                stage_logs<FIELD == 6, false, true>(R, x, y, z0, s0);
-            } else {
-              if (n_in == 0)
-                stage_logs<FIELD == 6, true, false>(R, x, y, z0, s0);
-              else
-                stage_logs<FIELD == 6, false, false>(R, x, y, z0, s0);
-            }
+            if (!kSplitAcc && wants_acc<FIELD>(R))
+              stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, s0);
+            else
+              stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, s0);
           }
-          // list entries are read one step ahead (past the end: harmless reads
-          // inside the CTA's shared memory, discarded)
-          int k = 1, off = off_at(1);
-          for (; k + 1 < n_tot; k += 2) {  // ping-pong: no state copies
-            const int off1 = off_at(k + 1);
-            step(k, off, s1, s0, w);
+          // list entries are read one step ahead (past the end: harmless
+          // reads inside the CTA's shared memory, discarded)
+          int k = 1, off = off_of(1);
+          for (; k + 1 < cnt; k += 2) {  // ping-pong: no state copies
+            const int off1 = off_of(k + 1);
+            step(off, s1, s0, w);
             push(w, s0.cw);
-            off = off_at(k + 2);
-            step(k + 1, off1, s0, s1, w);
+            off = off_of(k + 2);
+            step(off1, s0, s1, w);
             push(w, s1.cw);
           }
-          if (k < n_tot) {
-            step(k, off, s1, s0, w);
+          if (k < cnt) {
+            step(off, s1, s0, w);
             push(w, s0.cw);
             stage_exps(s1, w);
             push(w, s1.cw);
@@ -310,7 +298,9 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             stage_exps(s0, w);
             push(w, s0.cw);
           }
-        }
+        };
+        run(std::false_type{}, n_in, [&](int k) { return (int)lst[k] << 4; });
+        run(std::true_type{}, n_part, [&](int k) { return (int)lst[S::kChunk - 1 - k] << 4; });
         // strict: the accurate-log primitives after the rest, unpipelined
         // (their long FMA-pipe logs no longer double the pipelined loop's code)
         for (int k = 0; k < n_acc; ++k) {
