@@ -229,10 +229,15 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         n_part += __popc(mp);
       }
       __syncwarp();
+      // the operands are single-buffered: once a K step is issued, wait for
+      // its MMAs before the next primitive's stores (the wait overlaps the
+      // other warps' work; no per-primitive check for it)
       auto push = [&](const float(&w)[kVPT], float cw) {
-        if (kk == 0) wait_free();  // the previous step's MMAs must have read A/B
         store_k(kk, w, cw);
-        if (++kk == kK) issue();
+        if (++kk == kK) {
+          issue();
+          wait_free();
+        }
       };
       // class weight n = lane (sigma at CM), zero beyond
       auto class_weight = [&](int off) {
