@@ -283,16 +283,26 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             else
               stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, s0);
           }
+          // an even K slot at the loop head lets each two-primitive iteration
+          // check for a full K step once (pad with a zero column if odd)
+          if (kk & 1) {
+            const float zw[kVPT] = {0.f, 0.f, 0.f, 0.f};
+            push(zw, 0.0f);
+          }
           // list entries are read one step ahead (past the end: harmless
           // reads inside the CTA's shared memory, discarded)
           int k = 1, off = off_of(1);
           for (; k + 1 < cnt; k += 2) {  // ping-pong: no state copies
             const int off1 = off_of(k + 1);
             step(off, s1, s0, w);
-            push(w, s0.cw);
+            store_k(kk++, w, s0.cw);  // kk odd after this: the step cannot be full
             off = off_of(k + 2);
             step(off1, s0, s1, w);
-            push(w, s1.cw);
+            store_k(kk++, w, s1.cw);
+            if (kk == kK) {
+              issue();
+              wait_free();
+            }
           }
           if (k < cnt) {
             step(off, s1, s0, w);
