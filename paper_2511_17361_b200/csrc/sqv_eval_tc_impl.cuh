@@ -318,13 +318,16 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         run(std::true_type{}, n_part, [&](int k) { return (int)lst[S::kChunk - 1 - k] << 4; });
         // strict: the accurate-log primitives after the rest, unpipelined
         // (their long FMA-pipe logs no longer double the pipelined loop's code)
-        for (int k = 0; k < n_acc; ++k) {
-          const int off = (int)lst_acc[k] * S::kStride * 4;
-          const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
-          float w[kVPT];
-          pair_weights<FIELD, true>(R, x, y, z0, w);
-          push(w, class_weight(off));
-        }
+        if (kSplitAcc)
+          for (int k = 0; k < n_acc; ++k) {
+            const int off = (int)lst_acc[k] * S::kStride * 4;
+            const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
+            PairState st;
+            float w[kVPT];
+            stage_logs<true, true, true>(R, x, y, z0, st);  // exact steps, window test, acc logs
+            stage_exps(st, w);
+            push(w, class_weight(off));
+          }
       } else {
         for (int k = 0; k < n_tot; ++k) {
           const int off = off_at(k);
