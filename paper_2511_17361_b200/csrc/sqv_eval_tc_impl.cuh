@@ -261,16 +261,13 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         auto run = [&](auto live, int cnt, auto off_of) {
           constexpr bool LIVE = decltype(live)::value;
           if (cnt <= 0) return;
+          // (strict mode's accurate-log primitives are in lst_acc, so every
+          // primitive here takes the SFU logs: the step has no branch)
           auto step = [&](int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             nxt.cw = class_weight(off);
-            if (!kSplitAcc && wants_acc<FIELD>(R)) {
-              stage_exps<1>(cur, w);
-              stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, nxt);
-            } else {
-              stage_exps<2>(cur, w);
-              stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
-            }
+            stage_exps(cur, w);
+            stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
           };
           PairState s0, s1;
           float w[kVPT];
@@ -278,10 +275,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             const int off = off_of(0);
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             s0.cw = class_weight(off);
-            if (!kSplitAcc && wants_acc<FIELD>(R))
-              stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, s0);
-            else
-              stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, s0);
+            stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, s0);
           }
           // an even K slot at the loop head lets each two-primitive iteration
           // check for a full K step once (pad with a zero column if odd)

@@ -259,11 +259,7 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
 // Stage 2: log2(1 + t), S^b, Z, F and w = exp(-F).  w = 0 exactly once
 // -F log2(e) < -126 (ftz), i.e. for every F > kFCut — the same zero the block
 // cull assumes — so no select is needed (F is never NaN: see above).
-// (TAG only keeps per-branch copies distinct, so the compiler cannot sink
-// them out of the branches that also hold the next primitive's stage_logs.)
-template <int TAG = 0>
 __device__ __forceinline__ void stage_exps(const PairState& S, float (&w)[kVPT]) {
-  if (TAG) asm volatile("// stage_exps %0" ::"n"(TAG));
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float2 l1p = log2_1p_poly2(S.t[h]);
