@@ -405,8 +405,22 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
       if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, (int)T, ntx, nty, N,
                                       bmask, s))
         return rc;
-    if (int rc = ffma ? eval_launch(A, cm, (int)FT, s) : eval_tc_launch(A, cm, (int)FT, s))
-      return rc;
+    // The tensor cores accumulate with truncation: the bias grows with the
+    // number of K steps per voxel (measured: about -1e-8 relative per entry
+    // per tile, scripts/diag_depth.py).  Tiles deeper than the precision
+    // mode allows go to the CUDA-core evaluator (FP32 round-to-nearest),
+    // launched after the tensor-core one on the same stream.
+    int depth = cfg->precision ? 512 : 768;
+    if (const char* de = std::getenv("SQV_TC_DEPTH")) depth = std::atoi(de);
+    A.tc_max_entries = ffma ? -1 : depth;
+    A.ffma_min_entries = ffma ? -1 : depth;
+    if (ffma) {
+      if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
+    } else {
+      if (int rc = eval_tc_launch(A, cm, (int)FT, s)) return rc;
+      if (E > depth && cm <= 32)
+        if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
+    }
   }
   if (prof) {
     std::lock_guard<std::mutex> lk(g_prof.mu);

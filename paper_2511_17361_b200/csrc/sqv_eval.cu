@@ -52,7 +52,13 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
   float* s_lw = smem + kChunk * kRecWords;               // [kChunk][kLRow]
   unsigned* s_mask = reinterpret_cast<unsigned*>(s_lw + kChunk * S::kLRow);  // [kWarps][kMaskWords]
 
-  const int tile_g = blockIdx.x;
+  // One tile per CTA, or — as the deep-tile complement of the tensor-core
+  // evaluator — a grid-stride walk that takes only tiles with more than
+  // ffma_min_entries entries (the others are the tensor-core kernel's).
+  for (int tile_g = blockIdx.x; tile_g < A.n_tiles; tile_g += gridDim.x) {
+  if (A.ffma_min_entries >= 0 &&
+      A.tile_off[tile_g + 1] - A.tile_off[tile_g] <= A.ffma_min_entries)
+    continue;
   const int f = tile_g / A.tiles_per_frame;
   const int t = tile_g - f * A.tiles_per_frame;
   const int tx = t % A.ntx;
@@ -193,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
       }
     }
   }
+  }  // tile loop
 }
 
 template <int CM>
@@ -202,7 +209,18 @@ int launch_cm(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem) !=
       cudaSuccess)
     return check_launch("eval_kernel attribute");
-  kern<<<n_tiles, kThreads, S::kSmem, s>>>(A);
+  int grid = n_tiles;
+  if (A.ffma_min_entries >= 0) {  // deep tiles only: a grid-stride walk
+    static int n_sm = 0;
+    if (!n_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      if (n_sm < 1) n_sm = 148;
+    }
+    grid = n_tiles < 2 * n_sm ? n_tiles : 2 * n_sm;
+  }
+  kern<<<grid, kThreads, S::kSmem, s>>>(A);
   count_launch();
   return check_launch("eval_kernel");
 }

@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
 
   int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + kWarps * 4);
+  if (!PERSIST && A.tile_off[blockIdx.x + 1] - A.tile_off[blockIdx.x] > A.tc_max_entries)
+    return;  // a deep tile: the CUDA-core evaluator (launched next) owns it
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // ---- TMEM + barriers ----
@@ -192,7 +194,11 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     groups = 0;
     // claim the next tile now; the result is only needed at the epilogue
     const int claimed = (PERSIST && tid == 0) ? atomicAdd(A.tile_counter, 1) : 0;
-    const int beg = A.tile_off[tile_g], end = A.tile_off[tile_g + 1];
+    const int beg = A.tile_off[tile_g];
+    int end = A.tile_off[tile_g + 1];
+    // a deep tile is left to the CUDA-core evaluator (launched next, which
+    // overwrites the zeros written here)
+    if (end - beg > A.tc_max_entries) end = beg;
     const int64_t fbase = (int64_t)f * A.n_prims;
     for (int c0 = beg; c0 < end; c0 += S::kChunk) {
       const int n = min(S::kChunk, end - c0);
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     prefetched = false;
     if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
       const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
-      if (ne > nb) {
+      if (ne > nb && ne - nb <= A.tc_max_entries) {
         const int nf = next_tile / A.tiles_per_frame;
         stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
         prefetched = true;

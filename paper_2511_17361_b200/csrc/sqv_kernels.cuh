@@ -46,6 +46,11 @@ struct EvalArgs {
   float* v_o;
   float* v_c;
   int n_tiles;        // F * tiles per frame
+  // accumulation-depth split: the tensor-core evaluator takes tiles with at
+  // most tc_max_entries (tile, primitive) entries, the CUDA-core one those
+  // with more than ffma_min_entries (-1: all tiles)
+  int tc_max_entries;
+  int ffma_min_entries;
   int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
   int64_t n_entries;  // (tile, primitive) entries of the batch
   const uint16_t* bmask;  // per entry: bit b = may hit warp block b, bit 8+b = covers it

@@ -497,3 +497,29 @@ def test_run_many_two_stream_pipeline_matches_direct_calls():
     for (gl, gc), (wl, wc) in zip(got, want):
         np.testing.assert_array_equal(gl.cpu().numpy(), wl)
         np.testing.assert_array_equal(gc.cpu().numpy(), wc)
+
+
+@pytest.mark.parametrize("case", range(int(os.environ.get("SQV_RANDOM_DENSE_CASES", "8"))))
+def test_randomized_dense_configurations(case):
+    """Dense random scenes (hundreds of entries per tile: multi-chunk tiles,
+    many K steps, all three strict-mode passes) vs the oracle."""
+    P = _pkg()
+    rng = np.random.default_rng(5000 + case)
+    dims = (int(rng.integers(24, 72)), int(rng.integers(24, 72)), int(rng.choice([8, 16, 20])))
+    res = float(rng.choice([0.3, 0.4]))
+    origin = (-dims[0] * res / 2, -dims[1] * res / 2, -1.0)
+    C = int(rng.choice([5, 12, 18, 24]))
+    prec = "fast" if case % 3 == 2 else "strict"
+    mode = "prob-sum" if case % 4 == 3 else "logit-sum"
+    N = int(rng.integers(300, 1500))
+    spec = P.VoxelGridSpec(origin, dims, res)
+    cfg = P.VoxelizeConfig(semantic_mode=mode, precision=prec)
+    b = _scene(9000 + case, N, C, frames=2, origin=origin, dims=dims, resolution=res,
+               emin=float(rng.choice([0.1, 0.2])))
+    out = _run(b, spec, cfg, C, bins=True)
+    ref, grid = _oracle(b, spec, cfg, out["free_code"])
+    off, ids = O.bins(ref["windows"], grid.dims)
+    np.testing.assert_array_equal(out["tile_off"], off)
+    np.testing.assert_array_equal(out["prim_ids"], ids)
+    assert out["n_pairs"] == ref["n_pairs"]
+    assert_parity(out, ref, cfg.tau, out["free_code"], mode=prec)
