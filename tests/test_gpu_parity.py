@@ -516,7 +516,11 @@ def test_randomized_dense_configurations(case):
     cfg = P.VoxelizeConfig(semantic_mode=mode, precision=prec)
     b = _scene(9000 + case, N, C, frames=2, origin=origin, dims=dims, resolution=res,
                emin=float(rng.choice([0.1, 0.2])))
-    out = _run(b, spec, cfg, C, bins=True)
+    os.environ["SQV_PERSIST"] = str(case % 2)  # deep tiles in both evaluator modes
+    try:
+        out = _run(b, spec, cfg, C, bins=True)
+    finally:
+        del os.environ["SQV_PERSIST"]
     ref, grid = _oracle(b, spec, cfg, out["free_code"])
     off, ids = O.bins(ref["windows"], grid.dims)
     np.testing.assert_array_equal(out["tile_off"], off)
