@@ -12,6 +12,10 @@
                                                absolute, is amplified by
                                                2/eps1 <= 10 in F and by F in
                                                exp(-F); z steps are rounded once);
+* class sums v_c: twice the v_o bound per mode, against the voxel's weight
+  scale max(max_k |v_c,k|, v_o, floor) — with mixed-sign logits cancelling
+  inside v_c and sigma < 1 that scale is only a lower bound of the term
+  magnitude sum_i w_i |c_i|;
 * labels: a voxel may disagree only where the oracle's top-2 class scores
   differ by < LABEL_GAP * max(1, |top-1|), or where the oracle's v_o lies
   within VO_REL of tau (a tau flip); overall agreement >= 99.99%.
@@ -68,13 +72,14 @@ def label_check(gpu_lab, ref_lab, ref_vo, ref_vc, tau, free_code):
             "n_unexplained": len(unexplained), "agreement": agree}
 
 
-def assert_parity(gpu, ref, tau, free_code, check_vc=True, mode="strict"):
+def assert_parity(gpu, ref, tau, free_code, check_vc=True, mode="strict",
+                  min_agreement=MIN_AGREEMENT):
     """gpu/ref: dicts with v_o [F,V], v_c [F,V,C] (ref FP64), labels [F,V]."""
     vo = vo_check(gpu["v_o"], ref["v_o"], tau, mode)
     assert vo["n_bad"] == 0, f"v_o out of tolerance: {vo}"
     lab = label_check(gpu["labels"], ref["labels"], ref["v_o"], ref["v_c"], tau, free_code)
     assert lab["n_unexplained"] == 0, f"unexplained label mismatches: {lab}"
-    assert lab["agreement"] >= MIN_AGREEMENT, lab
+    assert lab["agreement"] >= min_agreement, lab
     if check_vc:
         # class weights: absolute error relative to the voxel's weight scale,
         # max(|v_c|, v_o) — v_o = sum(sigma w) bounds sum(w) from below, so it
@@ -82,7 +87,11 @@ def assert_parity(gpu, ref, tau, free_code, check_vc=True, mode="strict"):
         vc_g = np.asarray(gpu["v_c"], np.float64)
         vc_r = np.asarray(ref["v_c"], np.float64)
         vo_r = np.asarray(ref["v_o"], np.float64).reshape(vc_r.shape[:-1] + (1,))
-        scale = np.maximum(np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), vo_r), 1e-3)
+        floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
+        scale = np.maximum(np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), vo_r), floor)
         rel = np.abs(vc_g - vc_r) / scale
-        assert float(rel.max(initial=0.0)) <= 1e-4, f"v_c worst {float(rel.max())}"
+        # twice the v_o bound: max(|v_c|, v_o) only bounds the term magnitude
+        # sum(w |c|) from below when mixed-sign logits cancel (and sigma < 1)
+        lim = 2 * (VO_REL if mode == "strict" else VO_REL_TAIL)
+        assert float(rel.max(initial=0.0)) <= lim, f"v_c worst {float(rel.max())}"
     return vo, lab

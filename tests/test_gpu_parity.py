@@ -470,11 +470,8 @@ def test_randomized_configurations(case):
     np.testing.assert_array_equal(out["tile_off"], off)
     np.testing.assert_array_equal(out["prim_ids"], ids)
     assert out["n_pairs"] == ref["n_pairs"]
-    vo = vo_check(out["v_o"], ref["v_o"], cfg.tau, prec)
-    assert vo["n_bad"] == 0, vo
-    lab = label_check(out["labels"], ref["labels"], ref["v_o"], ref["v_c"], cfg.tau,
-                      out["free_code"])
-    assert lab["n_unexplained"] == 0, lab  # tiny grids: no agreement-rate floor
+    # tiny grids: no agreement-rate floor (every mismatch must be explained)
+    assert_parity(out, ref, cfg.tau, out["free_code"], mode=prec, min_agreement=0.0)
 
 
 def test_run_many_two_stream_pipeline_matches_direct_calls():
