@@ -40,7 +40,8 @@ struct Header {  // device-side scalars, read back in one 32-byte copy
   long long n_entries;
   unsigned long long bad_word;
   unsigned long long n_pairs;
-  long long pad;  // low word: the persistent evaluator's tile counter
+  int tile_counter;  // the persistent evaluator's work counter
+  int deep_count;    // tiles listed for the CUDA-core complement
 };
 
 // The one mid-pipeline readback goes through a mapped pinned buffer written
@@ -68,7 +69,7 @@ static Header* mapped_header() {
 }
 
 struct Layout {
-  size_t hdr, recs, lrows, counts, offs, windows, tile_off, scan_tmp;  // fixed
+  size_t hdr, recs, lrows, counts, offs, windows, tile_off, deep, scan_tmp;  // fixed
   size_t keys_a, vals_a, keys_b, vals_b, radix_tmp, bmask;                       // variable
   size_t fixed_end, total;
 };
@@ -88,6 +89,7 @@ Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
   L.offs = take((size_t)(FN + 1) * 4);
   L.windows = take((size_t)FN * 6 * 4);
   L.tile_off = take((size_t)(FT + 1) * 4);
+  L.deep = take((size_t)FT * 4);
   const int64_t st = scan_tmp_ints(FN > FT ? FN : FT);
   L.scan_tmp = take((size_t)st * 4);
   L.fixed_end = o;
@@ -363,7 +365,22 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   }
   const int* sorted_vals = which ? vals_b : vals_a;
   const uint32_t* sorted_keys = which ? keys_b : keys_a;
-  tile_bounds_kernel<<<div_up(FT + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off);
+  // evaluator choice: tcgen05 by default; SQV_EVAL=ffma selects the
+  // CUDA-core one (A/B runs).  The tensor cores accumulate with truncation:
+  // the bias grows with the number of K steps per voxel (measured: about
+  // -1e-8 relative per entry per tile, scripts/diag_depth.py).  Tiles deeper
+  // than the precision mode allows go to the CUDA-core evaluator (FP32
+  // round-to-nearest), launched after the tensor-core one on the same
+  // stream over the list tile_bounds_kernel builds.
+  const char* ev = std::getenv("SQV_EVAL");
+  const bool ffma = (ev && std::strcmp(ev, "ffma") == 0) || !eval_tc_supported(cm);
+  int depth = cfg->precision ? 512 : 768;
+  if (const char* de = std::getenv("SQV_TC_DEPTH")) depth = std::atoi(de);
+  const bool complement = !ffma && E > depth && cm <= 32;
+  int* deep = (int*)(ws + L.deep);
+  tile_bounds_kernel<<<div_up(FT + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off,
+                                                         complement ? depth : -1, deep,
+                                                         &hdr->deep_count);
   count_launch();
   if (int rc = check_launch("tile_bounds_kernel")) return rc;
   uint16_t* bmask = (uint16_t*)(ws + L.bmask);
@@ -393,32 +410,24 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.v_o = out->v_o;
   A.v_c = out->v_c;
   A.n_tiles = (int)FT;
-  A.tile_counter = reinterpret_cast<int*>(&hdr->pad);  // zeroed with the header
+  A.tile_counter = &hdr->tile_counter;  // zeroed with the header
+  A.deep_tiles = deep;
+  A.deep_count = &hdr->deep_count;
   A.n_entries = E;
   if (prof) cudaEventRecord(g_prof.ev[pset][3], s);
   {
-    // tcgen05 evaluator by default; SQV_EVAL=ffma selects the CUDA-core one (A/B runs)
-    const char* ev = std::getenv("SQV_EVAL");
-    const bool ffma = (ev && std::strcmp(ev, "ffma") == 0) || !eval_tc_supported(cm);
     A.bmask = bmask;
     if (!ffma && E > 0)
       if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, (int)T, ntx, nty, N,
                                       bmask, s))
         return rc;
-    // The tensor cores accumulate with truncation: the bias grows with the
-    // number of K steps per voxel (measured: about -1e-8 relative per entry
-    // per tile, scripts/diag_depth.py).  Tiles deeper than the precision
-    // mode allows go to the CUDA-core evaluator (FP32 round-to-nearest),
-    // launched after the tensor-core one on the same stream.
-    int depth = cfg->precision ? 512 : 768;
-    if (const char* de = std::getenv("SQV_TC_DEPTH")) depth = std::atoi(de);
     A.tc_max_entries = ffma ? -1 : depth;
     A.ffma_min_entries = ffma ? -1 : depth;
     if (ffma) {
       if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
     } else {
       if (int rc = eval_tc_launch(A, cm, (int)FT, s)) return rc;
-      if (E > depth && cm <= 32)
+      if (complement)
         if (int rc = eval_launch(A, cm, (int)FT, s)) return rc;
     }
   }

@@ -53,12 +53,13 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
   unsigned* s_mask = reinterpret_cast<unsigned*>(s_lw + kChunk * S::kLRow);  // [kWarps][kMaskWords]
 
   // One tile per CTA, or — as the deep-tile complement of the tensor-core
-  // evaluator — a grid-stride walk that takes only tiles with more than
-  // ffma_min_entries entries (the others are the tensor-core kernel's).
-  for (int tile_g = blockIdx.x; tile_g < A.n_tiles; tile_g += gridDim.x) {
-  if (A.ffma_min_entries >= 0 &&
-      A.tile_off[tile_g + 1] - A.tile_off[tile_g] <= A.ffma_min_entries)
-    continue;
+  // evaluator — a grid-stride walk over the tiles with more than
+  // ffma_min_entries entries, listed by tile_bounds_kernel (the others are
+  // the tensor-core kernel's).
+  const bool listed = A.ffma_min_entries >= 0;
+  const int n_walk = listed ? *A.deep_count : A.n_tiles;
+  for (int it = blockIdx.x; it < n_walk; it += gridDim.x) {
+  const int tile_g = listed ? A.deep_tiles[it] : it;
   const int f = tile_g / A.tiles_per_frame;
   const int t = tile_g - f * A.tiles_per_frame;
   const int tx = t % A.ntx;

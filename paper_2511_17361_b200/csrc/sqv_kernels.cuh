@@ -48,9 +48,11 @@ struct EvalArgs {
   int n_tiles;        // F * tiles per frame
   // accumulation-depth split: the tensor-core evaluator takes tiles with at
   // most tc_max_entries (tile, primitive) entries, the CUDA-core one those
-  // with more than ffma_min_entries (-1: all tiles)
+  // with more than ffma_min_entries (-1: all tiles), listed by tile_bounds_kernel
   int tc_max_entries;
   int ffma_min_entries;
+  const int* deep_tiles;  // tiles with more than ffma_min_entries entries (unordered)
+  const int* deep_count;  // their number (device)
   int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
   int64_t n_entries;  // (tile, primitive) entries of the batch
   const uint16_t* bmask;  // per entry: bit b = may hit warp block b, bit 8+b = covers it
@@ -65,7 +67,8 @@ int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64
 __global__ void prep_kernel(PrepArgs A);
 __global__ void emit_kernel(EmitArgs A);
 __global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
-                                   int* tile_off);
+                                   int* tile_off, int deep_min, int* deep_tiles,
+                                   int* deep_count);
 
 // exclusive scan of n int32 values; out has n+1 entries (out[n] = total);
 // if total64 != nullptr the total is also stored there.  tmp needs

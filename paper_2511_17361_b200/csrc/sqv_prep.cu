@@ -195,14 +195,10 @@ __global__ void emit_kernel(EmitArgs A) {
   }
 }
 
-// tile_off[t] = first sorted entry with key >= t (t = 0 .. n_tiles): one
-// thread per tile, a binary search over the sorted keys (the upper levels
-// stay in L2/L1 for every thread).
-__global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
-                                   int* tile_off) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > n_tiles) return;
-  int64_t lo = 0, hi = n;  // first index in [lo, hi) with keys[idx] >= t
+// First sorted entry with key >= t (the upper levels of the search stay in
+// L2/L1 for every thread).
+__device__ __forceinline__ int64_t lower_bound_key(const uint32_t* keys, int64_t n, int64_t t) {
+  int64_t lo = 0, hi = n;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
     if ((int64_t)__ldg(keys + mid) < t)
@@ -210,7 +206,24 @@ __global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_ti
     else
       hi = mid;
   }
-  tile_off[t] = (int)lo;
+  return lo;
+}
+
+// tile_off[t] = first sorted entry with key >= t (t = 0 .. n_tiles), one
+// thread per tile.  With deep_min >= 0, tiles holding more than deep_min
+// entries are also appended (unordered) to deep_tiles: the CUDA-core
+// evaluator's complement walks that list instead of every tile.
+__global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_tiles,
+                                   int* tile_off, int deep_min, int* deep_tiles,
+                                   int* deep_count) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lo = lower_bound_key(keys, n, t < n_tiles ? t : n_tiles);
+  if (t <= n_tiles) tile_off[t] = (int)lo;
+  if (deep_min < 0) return;
+  // the next tile's offset: the neighbour lane's, searched by the last lane
+  int64_t nxt = __shfl_down_sync(0xffffffffu, lo, 1);
+  if ((threadIdx.x & 31) == 31) nxt = lower_bound_key(keys, n, t + 1 < n_tiles ? t + 1 : n_tiles);
+  if (t < n_tiles && nxt - lo > deep_min) deep_tiles[atomicAdd(deep_count, 1)] = (int)t;
 }
 
 }  // namespace sqv
