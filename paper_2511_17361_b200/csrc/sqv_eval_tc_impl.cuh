@@ -73,7 +73,11 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + kWarps * 4);
   if (!PERSIST && A.tile_off[blockIdx.x + 1] - A.tile_off[blockIdx.x] > A.tc_max_entries)
     return;  // a deep tile: the CUDA-core evaluator (launched next) owns it
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index and TMEM base through a lane-0 shuffle: provably warp-uniform
+  // for ptxas, so the MMA operands derived from them live in uniform
+  // registers (no per-issue elect/broadcast loops)
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
   // ---- TMEM + barriers ----
   if (warp == 0) {
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tmem_base = *s_tmem;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *s_tmem, 0);
   const uint32_t d_tmem = tmem_base + (uint32_t)(warp * kN);
 
   uint8_t* a_hi = smem + S::kA + warp * 8192;
@@ -142,13 +146,9 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   auto issue = [&]() {
     tc::fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      tc::fence_after_sync();
-      tc::mma_tf32(d_tmem, da_hi, db_hi, kIdesc, groups > 0 ? 1u : 0u);
-      tc::mma_tf32(d_tmem, da_hi, db_lo, kIdesc, 1u);
-      tc::mma_tf32(d_tmem, da_lo, db_hi, kIdesc, 1u);
-      tc::mma_commit(&s_bar[warp]);
-    }
+    tc::fence_after_sync();
+    tc::mma3_tf32_commit(d_tmem, da_hi, da_lo, db_hi, db_lo, kIdesc, groups == 0 ? 1u : 0u,
+                         &s_bar[warp]);
     __syncwarp();
     ++groups;
     pending = true;

@@ -109,6 +109,26 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// One K step of the 3xTF32 split (hi*hi + hi*lo + lo*hi) and its commit,
+// issued by one elected lane of the calling (converged) warp: elect.sync
+// inside the asm, so ptxas needs no per-instruction elect loop.  `first`
+// = 1 starts the accumulator (enable-input-d off for the first MMA).
+__device__ __forceinline__ void mma3_tf32_commit(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo,
+                                                 uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
+                                                 uint32_t first, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, acc;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.b32 acc, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, acc;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n}" ::"r"(
+          d_tmem),
+      "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(first), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Instruction descriptor: D f32, A/B tf32, M x N; a_mn/b_mn select
 // MN-major operands (bits 15/16).
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
