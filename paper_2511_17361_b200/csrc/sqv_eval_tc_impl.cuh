@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           auto step = [&](int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             nxt.cw = class_weight(off);
-            stage_exps(cur, w);
+            stage_exps<FIELD == 7>(cur, w);
             stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
           };
           PairState s0, s1;
@@ -312,10 +312,10 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           if (k < cnt) {
             step(off, s1, s0, w);
             push(w, s0.cw);
-            stage_exps(s1, w);
+            stage_exps<FIELD == 7>(s1, w);
             push(w, s1.cw);
           } else {
-            stage_exps(s0, w);
+            stage_exps<FIELD == 7>(s0, w);
             push(w, s0.cw);
           }
         };
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             PairState st;
             float w[kVPT];
             stage_logs<true, true, true>(R, x, y, z0, st);  // exact steps, window test, acc logs
-            stage_exps(st, w);
+            stage_exps<FIELD == 7>(st, w);
             push(w, class_weight(off));
           }
       } else {
