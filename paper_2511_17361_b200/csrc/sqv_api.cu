@@ -43,6 +43,7 @@ struct Header {  // device-side scalars, read back in one 32-byte copy
   int tile_counter;  // the persistent evaluator's work counter
   int deep_count;    // tiles listed for the CUDA-core complement
 };
+static_assert(sizeof(Header) == 4 * sizeof(long long), "header_out_kernel copies 4 words");
 
 // The one mid-pipeline readback goes through a mapped pinned buffer written
 // by a one-thread kernel: no copy engine is involved, so the readback never
