@@ -264,7 +264,10 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
     S.um[h] = make_float2(fmaxf(ux.x, uy.x), fmaxf(ux.y, uy.y));
     const float2 dd = add2(ux, make_float2(-uy.x, -uy.y));
     const float2 d = make_float2(fmaxf(-fabsf(dd.x), -126.0f), fmaxf(-fabsf(dd.y), -126.0f));
-    if (SQV_EXP_POLY >= 2)
+    // fast mode takes one voxel pair's t on the FMA pipe (+1.4%: the SFU
+    // binds there; strict, whose accurate logs load the FMA pipe, is neutral
+    // with it and -1.1% with both pairs' t there, so it keeps the SFU)
+    if (SQV_EXP_POLY >= 2 || (!EXACT_STEP && h == 0))
       S.t[h] = ex2_poly2(d);
     else
       S.t[h] = make_float2(ex2(d.x), ex2(d.y));
