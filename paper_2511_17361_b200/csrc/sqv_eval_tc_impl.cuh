@@ -27,7 +27,11 @@ template <int CM>
 struct TcShape {
   static_assert(CM + 1 <= kN, "sigma column must fit in N");
   static constexpr int kLRow = (CM + 1 + 3) & ~3;
+#ifdef SQV_CHUNK
+  static constexpr int kChunk = CM <= 18 ? SQV_CHUNK : 104;
+#else
   static constexpr int kChunk = CM <= 18 ? 120 : 104;
+#endif
   // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
   static constexpr int kA = 0;
   static constexpr int kB = kA + kWarps * 2 * 4096;
