@@ -157,14 +157,18 @@ class ClockSampler:
 # CPU legs (oracle: test/baseline infrastructure only)
 # ---------------------------------------------------------------------------
 
-def cpu_run(a, max_frames, budget_s):
-    """Time the FP64 oracle (all host threads) on frames of the same workload
-    until budget_s elapses or max_frames frames are done.  Returns
-    (frames/s, frames, seconds, threads, pairs/s)."""
+def cpu_run(a, max_frames, budget_s, threads=None):
+    """Time the FP64 oracle (all host threads, or `threads`) on frames of the
+    same workload until budget_s elapses or max_frames frames are done.
+    Returns (frames/s, frames, seconds, threads, pairs/s)."""
     from oracle import oracle as O
     from paper_2511_17361_b200.scenegen import gen_frames
     O.build()
-    threads = O.threads()
+    all_threads = O.threads()
+    if threads is not None:
+        O.set_threads(threads)
+    else:
+        threads = all_threads
     grid, cfg = O.Grid(**a.grid), O.Cfg()
     done, pairs, t_total = 0, 0, 0.0
     while done < max_frames and (t_total < budget_s or done == 0):
@@ -174,6 +178,7 @@ def cpu_run(a, max_frames, budget_s):
         t_total += time.perf_counter() - t0
         pairs += r["n_pairs"]
         done += 1
+    O.set_threads(all_threads)
     return done / t_total, done, t_total, threads, pairs / t_total
 
 
@@ -407,9 +412,12 @@ def run_ours(a, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         fps, nfr, secs, thr, pps = cpu_run(a, 8, a.cpu_seconds)
+        fps1, nfr1, secs1, _, pps1 = cpu_run(a, 1, 0.0, threads=1)
         cpu = {"value": fps, "unit": UNIT, "cores": thr, "kind": "port",
                "sample": f"{nfr} frames of the config-2 workload in {secs:.1f} s, FP64 C oracle "
-                         f"(oracle/sqv_oracle.c), OpenMP {thr} threads; {pps:.3e} pairs/s"}
+                         f"(oracle/sqv_oracle.c), OpenMP {thr} threads; {pps:.3e} pairs/s",
+               "single_thread": {"value": fps1, "unit": UNIT, "pairs_per_s": pps1,
+                                 "sample": f"{nfr1} frame in {secs1:.1f} s, 1 thread"}}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
