@@ -94,7 +94,7 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
   const bool iz[2] = {z0 >= lo[2] && z0 + 7 <= hi[2], z0 + 8 >= lo[2] && z0 + 15 <= hi[2]};
   // sure-hit radius: (2^b + 1) M^c <= 0.5 kFCut  <=>  M <= (0.5 kFCut / (2^b + 1))^(1/c)
   const float inv_c = 1.0f / R.c;
-  const float sure = ex2(inv_c * lg2(0.5f * kFCut / (ex2(R.b) + 1.0f)));
+  const float sure = ex2(inv_c * lg2(0.5f * kBlockCut / (ex2(R.b) + 1.0f)));
   unsigned m = 0;
 #pragma unroll
   for (int bb = 0; bb < kWarps; ++bb) {
@@ -115,7 +115,7 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
     if (!hit) {
       const float F = field_F(fmaxf(mm[0] - eps, 0.0f), fmaxf(mm[1] - eps, 0.0f),
                               fmaxf(mm[2] - eps, 0.0f), R.a, R.b, R.c);
-      hit = F < 1.02f * kFCut;
+      hit = F < 1.02f * kBlockCut;
     }
     if (hit) m |= (1u << bb) | ((unsigned)(ix[ox] && iy[oy] && iz[oz]) << (8 + bb));
   }

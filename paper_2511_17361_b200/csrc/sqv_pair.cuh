@@ -39,7 +39,7 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
   // culled pair would have had F > kFCut, i.e. w = 0 exactly.
   const float F = field_F(fmaxf(m[0] - e, 0.0f), fmaxf(m[1] - e, 0.0f), fmaxf(m[2] - e, 0.0f),
                           R.a, R.b, R.c);
-  return F < 1.02f * kFCut;
+  return F < 1.02f * kBlockCut;
 }
 
 // Is the warp's whole 4x4x8 block inside R's window?  Then no voxel of the

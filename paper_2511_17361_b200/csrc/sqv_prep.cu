@@ -121,7 +121,7 @@ __device__ __forceinline__ int64_t prep_prim(const PrepArgs& A, int64_t gi) {
         rec.c = (float)(2.0 / P.e1);
         // F >= max(|x'|)^(2/e1): cull when max|x'| > kFCut^(e1/2) (+0.1% margin)
         // (exp2 of 0.5 e1 log2(kFCut); the 0.1% margin dwarfs its ulp error)
-        rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * 6.448512845609085) * 1.001);
+        rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * log2((double)SQV_BLOCK_CUT)) * 1.001);
         rec.cx = (float)cref[0];
         rec.cy = (float)cref[1];
         rec.cz = (float)cref[2];
