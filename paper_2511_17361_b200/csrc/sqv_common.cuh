@@ -22,16 +22,20 @@ constexpr float kFCap = 1e30f;   // core.py:23 (reported F only)
 constexpr float kFCut = 87.3365f;
 // Block-cull threshold (block masks and the Chebyshev bound mcut): a warp
 // block is skipped for a primitive when a conservative lower bound of F over
-// the block exceeds kBlockCut, i.e. every dropped weight is below
-// exp(-36) = 2.3e-16.  Even if all 8,000 primitives of the largest config
-// were dropped at one voxel that is < 2e-12 of v_o, 50x below the smallest
-// absolute tolerance of the parity bound (1e-5 x the 1e-5 floor).  Measured:
-// +11% over culling at kFCut (which drops nothing FP32 keeps).  SQV_BLOCK_CUT
-// is the dev knob (87.3365 restores the bit-faithful cull).
+// the block exceeds the primitive's cut = max(kBlockCutMin, ln(N wmax /
+// 2e-12)), N = primitives per frame, wmax = max(1, max |class weight|).
+// Every dropped weight is then below exp(-cut) <= 2e-12 / (N wmax), so at any
+// voxel the dropped v_o and each dropped v_c sum to < 2e-12 — 50x below the
+// smallest absolute tolerance of the parity bound (1e-5 x the 1e-5 floor).
+// For N <= 8,000 and |class weights| <= 1 the cut is 36 (exp(-36) =
+// 2.3e-16).  Measured: +11% over culling at kFCut (which drops nothing FP32
+// keeps).  SQV_BLOCK_CUT overrides the minimum (87.3365 restores the cull
+// that changes no output bit).
 #ifndef SQV_BLOCK_CUT
 #define SQV_BLOCK_CUT 36.0
 #endif
-constexpr float kBlockCut = (float)(SQV_BLOCK_CUT);
+constexpr double kBlockCutMin = SQV_BLOCK_CUT;
+constexpr double kLnInvDropBound = 26.937873;  // ln(1 / 2e-12)
 constexpr float kLog2e = 1.4426950408889634f;
 
 constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;

@@ -19,8 +19,9 @@
 //   F  = (|x'0|^a + |x'1|^a)^b + |x'2|^c          — 7 MUFU (field_F7)
 //   w  = exp(-F) (0 for F >= kFCut)               — 1 MUFU
 //   v_o += sigma*w; v_c[k] += w*c_k               — C+1 FFMA, in registers
-// Culling (never changes an output bit, see kFCut): skipped when every live
-// voxel of the warp has max|x'| > mcut, i.e. F > kFCut.
+// Culling (block_may_hit): skipped when F exceeds the primitive's block-cull
+// threshold on every voxel of the warp's block (every dropped weight is below
+// exp(-cut); see kBlockCutMin in sqv_common.cuh).
 // Epilogue = finalize: free if v_o < tau, else the first
 // argmax; dense grids and labels staged through shared memory and written
 // as coalesced row segments (x-fastest layout).

@@ -46,9 +46,9 @@ namespace {
 // overlap, the Chebyshev box bound, the nearest-corner field bound, all
 // conservative); the shared parts are computed once per entry (local block
 // centres differ by fixed lattice steps), and a block whose nearest local
-// corner is deep inside — (2^b + 1) max|x'|^c well below kFCut — is marked
-// without the 8-MUFU field test.  A "hit" that could have been culled only
-// costs evaluation work: those pairs still get w = 0 exactly.
+// corner is deep inside — (2^b + 1) max|x'|^c well below the primitive's cut
+// — is marked without the 8-MUFU field test.  A "hit" that could have been
+// culled only costs evaluation work: those pairs get their exact FP32 w.
 __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t n,
                                    const float* recs, int tiles_per_frame, int ntx, int nty,
                                    int n_prims, uint16_t* bmask) {
@@ -83,6 +83,7 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
   }
   const float eps = 1e-4f * span;  // FP32 error of c, h (incl. the stepped centres)
   const float cut = R.mcut + eps;
+  const float cut_f = ex2(R.c * lg2(R.mcut));  // the primitive's field threshold (>= its cut)
   // window overlap / containment of the two block positions on each axis
   const int* lo = R.lo;
   const int* hi = R.hi;
@@ -94,7 +95,7 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
   const bool iz[2] = {z0 >= lo[2] && z0 + 7 <= hi[2], z0 + 8 >= lo[2] && z0 + 15 <= hi[2]};
   // sure-hit radius: (2^b + 1) M^c <= 0.5 kFCut  <=>  M <= (0.5 kFCut / (2^b + 1))^(1/c)
   const float inv_c = 1.0f / R.c;
-  const float sure = ex2(inv_c * lg2(0.5f * kBlockCut / (ex2(R.b) + 1.0f)));
+  const float sure = ex2(inv_c * lg2(0.5f * cut_f / (ex2(R.b) + 1.0f)));
   unsigned m = 0;
 #pragma unroll
   for (int bb = 0; bb < kWarps; ++bb) {
@@ -115,7 +116,7 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
     if (!hit) {
       const float F = field_F(fmaxf(mm[0] - eps, 0.0f), fmaxf(mm[1] - eps, 0.0f),
                               fmaxf(mm[2] - eps, 0.0f), R.a, R.b, R.c);
-      hit = F < 1.02f * kBlockCut;
+      hit = F < 1.02f * cut_f;
     }
     if (hit) m |= (1u << bb) | ((unsigned)(ix[ox] && iy[oy] && iz[oz]) << (8 + bb));
   }

@@ -11,8 +11,9 @@ constexpr int kVPT = 4;  // voxels per thread: a 1x1x4 z-column
 // Can primitive R contribute to the warp's 4x4x8 voxel block at (bx0, by0,
 // bz0)?  Window overlap, then conservative geometric tests: the block's
 // centre in local coordinates minus its local half extent must come within
-// mcut on every axis (else max|x'| > mcut on the whole block, F > kFCut),
-// and the field at the nearest corner of that local box must be below kFCut.
+// mcut on every axis (else max|x'| > mcut on the whole block, F > the
+// primitive's cut), and the field at the nearest corner of that local box
+// must be below the cut (recovered as mcut^c; see kBlockCutMin).
 // Evaluated lane-parallel (one primitive per lane) when building the masks.
 __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0, int bz0) {
   if (bx0 + 3 < R.lo[0] || bx0 > R.hi[0] || by0 + 3 < R.lo[1] || by0 > R.hi[1] ||
@@ -35,11 +36,11 @@ __device__ __forceinline__ bool block_may_hit(const PrimRec& R, int bx0, int by0
   if (dmax > R.mcut + e) return false;
   // Tighter: F grows with each |x'_r|, so over the block F >= F at the
   // box corner nearest the centre, |x'_r| >= max(|c_r| - h_r, 0).  Culled
-  // only with a 2% margin over kFCut, far above the SFU field error, so every
-  // culled pair would have had F > kFCut, i.e. w = 0 exactly.
+  // only with a 2% margin over the cut, far above the SFU field error, so
+  // every culled pair has F > cut, i.e. w < exp(-cut).
   const float F = field_F(fmaxf(m[0] - e, 0.0f), fmaxf(m[1] - e, 0.0f), fmaxf(m[2] - e, 0.0f),
                           R.a, R.b, R.c);
-  return F < 1.02f * kBlockCut;
+  return F < 1.02f * ex2(R.c * lg2(R.mcut));  // the primitive's field threshold
 }
 
 // Is the warp's whole 4x4x8 block inside R's window?  Then no voxel of the

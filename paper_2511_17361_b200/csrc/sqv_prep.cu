@@ -119,13 +119,11 @@ __device__ __forceinline__ int64_t prep_prim(const PrepArgs& A, int64_t gi) {
         rec.a = (float)(2.0 / P.e2);
         rec.b = (float)(P.e2 / P.e1);
         rec.c = (float)(2.0 / P.e1);
-        // F >= max(|x'|)^(2/e1): cull when max|x'| > kFCut^(e1/2) (+0.1% margin)
-        // (exp2 of 0.5 e1 log2(kFCut); the 0.1% margin dwarfs its ulp error)
-        rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * log2((double)SQV_BLOCK_CUT)) * 1.001);
         rec.cx = (float)cref[0];
         rec.cy = (float)cref[1];
         rec.cz = (float)cref[2];
         // class weights: logits (logit-sum) or softmax (prob-sum)
+        double wmax = 1.0;  // max(1, sigma, max_k |class weight|)
         if (A.cfg.semantic_mode == 1) {
           double m = logits[0];
           for (int k = 1; k < C; ++k) m = fmax(m, logits[k]);
@@ -133,8 +131,20 @@ __device__ __forceinline__ int64_t prep_prim(const PrepArgs& A, int64_t gi) {
           for (int k = 0; k < C; ++k) s += exp(logits[k] - m);
           for (int k = 0; k < C; ++k) lrow[k] = (float)(exp(logits[k] - m) / s);
         } else {
-          for (int k = 0; k < C; ++k) lrow[k] = (float)logits[k];
+          for (int k = 0; k < C; ++k) {
+            lrow[k] = (float)logits[k];
+            wmax = fmax(wmax, fabs(logits[k]));
+          }
         }
+        // Block-cull threshold of this primitive (sqv_common.cuh, kBlockCutMin):
+        // cut = max(36, ln(N wmax / 2e-12)), so the primitive's dropped weights,
+        // times its largest class weight, sum to < 2e-12 / N per voxel.
+        // F >= max(|x'|)^(2/e1): the Chebyshev bound culls when max|x'| >
+        // cut^(e1/2) (+0.1% margin, which dwarfs the exp2/log2 ulp error);
+        // the block masks recover the field threshold as mcut^c >= cut.
+        const double cut = fmax((double)kBlockCutMin,
+                                log((double)A.n_prims * wmax) + kLnInvDropBound);
+        rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * log2(cut)) * 1.001);
         for (int k = C; k < A.lrow; ++k) lrow[k] = 0.0f;
         lrow[A.cm] = (float)P.sigma;
         lrow_done = true;
