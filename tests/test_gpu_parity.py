@@ -524,3 +524,23 @@ def test_randomized_dense_configurations(case):
     np.testing.assert_array_equal(out["prim_ids"], ids)
     assert out["n_pairs"] == ref["n_pairs"]
     assert_parity(out, ref, cfg.tau, out["free_code"], mode=prec)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e6, 1e9])
+def test_block_cull_bound_with_large_logits(scale):
+    """The block cull drops weights below exp(-cut) with a per-primitive cut
+    = max(36, ln(N wmax / 2e-12)) (sqv_common.cuh kBlockCutMin): with small
+    primitives (most window voxels deep in the tail, F in 36..87), tau = 0
+    (every voxel labelled, tail voxels included) and logits scaled up to
+    1e9, v_o, v_c and labels still meet the parity bound."""
+    P = _pkg()
+    from paper_2511_17361_b200.core import PrimitiveBatch
+    origin, dims, res = (-8.0, -8.0, -1.0), (40, 40, 16), 0.4
+    spec = P.VoxelGridSpec(origin, dims, res)
+    cfg = P.VoxelizeConfig(tau=0.0, neighborhood_radius=5, semantic_mode="logit-sum")
+    b = _scene(4242, 60, 18, origin=origin, dims=dims, resolution=res, smax=0.6)
+    b = PrimitiveBatch(b.mu, b.scale, b.rot, b.opacity, b.eps, b.logits * scale)
+    out = _run(b, spec, cfg, 18)
+    ref, _ = _oracle(b, spec, cfg, out["free_code"])
+    assert out["n_pairs"] == ref["n_pairs"]
+    assert_parity(out, ref, cfg.tau, out["free_code"], min_agreement=0.0)
