@@ -419,8 +419,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   {
     A.bmask = bmask;
     if (!ffma && E > 0)
-      if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, (int)T, ntx, nty, N,
-                                      bmask, s))
+      if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, lrows, lrow, tile_off,
+                                      (int)T, ntx, nty, N, bmask, s))
         return rc;
     A.tc_max_entries = ffma ? -1 : depth;
     A.ffma_min_entries = ffma ? -1 : depth;

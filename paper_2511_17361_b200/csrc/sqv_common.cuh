@@ -28,8 +28,11 @@ constexpr float kFCut = 87.3365f;
 // voxel the dropped v_o and each dropped v_c sum to < 2e-12 — 50x below the
 // smallest absolute tolerance of the parity bound (1e-5 x the 1e-5 floor).
 // For N <= 8,000 and |class weights| <= 1 the cut is 36 (exp(-36) =
-// 2.3e-16).  Measured: +11% over culling at kFCut (which drops nothing FP32
-// keeps).  SQV_BLOCK_CUT overrides the minimum (87.3365 restores the cull
+// 2.3e-16).  The block masks (tensor-core path) tighten it per tile to
+// ln(E_tile wmax / 2e-12), E_tile = the tile's entries (~33 on config 2),
+// with the same per-voxel bound.  Measured: +11% (+1.4% more per tile) over
+// culling at kFCut (which drops nothing FP32 keeps).  SQV_BLOCK_CUT overrides
+// the prep minimum (87.3365 with the per-tile term removed restores the cull
 // that changes no output bit).
 #ifndef SQV_BLOCK_CUT
 #define SQV_BLOCK_CUT 36.0

@@ -50,7 +50,8 @@ namespace {
 // — is marked without the 8-MUFU field test.  A "hit" that could have been
 // culled only costs evaluation work: those pairs get their exact FP32 w.
 __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t n,
-                                   const float* recs, int tiles_per_frame, int ntx, int nty,
+                                   const float* recs, const float* lrows, int lrow,
+                                   const int* tile_off, int tiles_per_frame, int ntx, int nty,
                                    int n_prims, uint16_t* bmask) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -83,7 +84,15 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
   }
   const float eps = 1e-4f * span;  // FP32 error of c, h (incl. the stepped centres)
   const float cut = R.mcut + eps;
-  const float cut_f = ex2(R.c * lg2(R.mcut));  // the primitive's field threshold (>= its cut)
+  // The field threshold of this (tile, primitive) entry.  At most E_tile
+  // primitives reach a voxel of this tile, so cut = ln(E_tile wmax / 2e-12)
+  // keeps the dropped mass per voxel < 2e-12 (wmax rides in the class-weight
+  // row's padding column, written by prep; +0.01 covers __logf's error).
+  // The primitive's own (N-based) threshold mcut^c is the upper limit.
+  const float wmax = __ldg(lrows + ((int64_t)f * n_prims + ids[e]) * lrow + (lrow - 1));
+  const int e_tile = __ldg(tile_off + key + 1) - __ldg(tile_off + key);
+  const float cut_f = fminf(ex2(R.c * lg2(R.mcut)),
+                            __logf((float)e_tile * wmax) + (float)kLnInvDropBound + 0.01f);
   // window overlap / containment of the two block positions on each axis
   const int* lo = R.lo;
   const int* hi = R.hi;
@@ -128,11 +137,13 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
 bool eval_tc_supported(int cm) { return cm <= 24; }
 
 int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
-                       const float* recs, int tiles_per_frame, int ntx, int nty, int n_prims,
-                       uint16_t* bmask, cudaStream_t s) {
+                       const float* recs, const float* lrows, int lrow, const int* tile_off,
+                       int tiles_per_frame, int ntx, int nty, int n_prims, uint16_t* bmask,
+                       cudaStream_t s) {
   if (n_entries <= 0) return SQV_OK;
   block_masks_kernel<<<(unsigned)((n_entries + 127) / 128), 128, 0, s>>>(
-      sorted_keys, sorted_ids, n_entries, recs, tiles_per_frame, ntx, nty, n_prims, bmask);
+      sorted_keys, sorted_ids, n_entries, recs, lrows, lrow, tile_off, tiles_per_frame, ntx, nty,
+      n_prims, bmask);
   count_launch();
   return check_launch("block_masks_kernel");
 }

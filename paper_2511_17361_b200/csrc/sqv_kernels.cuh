@@ -61,8 +61,9 @@ struct EvalArgs {
 // per (tile, primitive) entry: the 8 warp-block tests of the tensor-core
 // evaluator (block_may_hit / block_inside), computed once, in parallel
 int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
-                       const float* recs, int tiles_per_frame, int ntx, int nty, int n_prims,
-                       uint16_t* bmask, cudaStream_t s);
+                       const float* recs, const float* lrows, int lrow, const int* tile_off,
+                       int tiles_per_frame, int ntx, int nty, int n_prims, uint16_t* bmask,
+                       cudaStream_t s);
 
 __global__ void prep_kernel(PrepArgs A);
 __global__ void emit_kernel(EmitArgs A);

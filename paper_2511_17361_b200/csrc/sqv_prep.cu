@@ -147,6 +147,9 @@ __device__ __forceinline__ int64_t prep_prim(const PrepArgs& A, int64_t gi) {
         rec.mcut = __double2float_ru(exp2(0.5 * P.e1 * log2(cut)) * 1.001);
         for (int k = C; k < A.lrow; ++k) lrow[k] = 0.0f;
         lrow[A.cm] = (float)P.sigma;
+        // the padding column (never read as a class) carries wmax for the
+        // block masks' per-tile cut (rounded up: the bound stays conservative)
+        lrow[A.lrow - 1] = __double2float_ru(wmax);
         lrow_done = true;
       }
     }
