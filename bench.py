@@ -333,7 +333,7 @@ def run_ours(a, rank, world, local_rank):
     eval_s = prof["eval_ms"] * 1e-3 / max(prof["calls"], 1)
     pairs_per_launch = pairs / max(K, 1)
     achieved = pairs_per_launch * MUFU_PER_PAIR / eval_s
-    traffic, traffic_src = None, None
+    traffic, traffic_src, sfu_busy = None, None, None
     try:  # DRAM bytes of the evaluator from the committed ncu --set full capture, per launch
         import glob
         ppath = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_eval_tc_ncu.json")))[-1]
@@ -341,11 +341,17 @@ def run_ours(a, rank, world, local_rank):
         traffic = (pj["dram_bytes_read"] + pj["dram_bytes_write"]) * B / pj["frames_per_launch"]
         traffic_src = (os.path.relpath(ppath, ROOT) +
                        f" (ncu {pj['frames_per_launch']}-frame launch, scaled to {B})")
+        sfu_busy = {"frac": pj["xu_pct"] / 100.0, "issue_frac": pj["issue_pct"] / 100.0,
+                    "source": os.path.relpath(ppath, ROOT),
+                    "note": "MUFU ops actually issued (ncu sm__inst_executed_pipe_xu): frac "
+                            "counts 9 MUFU for every in-window pair, the kernel issues 7 per "
+                            "evaluated pair and skips warp blocks whose F exceeds the cull "
+                            "threshold (< 2e-12 dropped per voxel), so frac can pass 1"}
     except Exception:
         pass
     roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                 "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": traffic,
-                "traffic_source": traffic_src,
+                "traffic_source": traffic_src, "sfu_busy_ncu": sfu_busy,
                 "algorithmic_bytes_per_launch": B * spec.n_voxels * (1 + 4 + 4 * C),
                 "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc_impl.cuh)" if os.environ.get(
                     "SQV_EVAL") != "ffma" else "eval_kernel (FFMA, sqv_eval.cu)",
