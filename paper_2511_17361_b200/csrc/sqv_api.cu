@@ -307,12 +307,16 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     P.windows = windows;
     P.bad_word = &hdr->bad_word;
     P.n_pairs = &hdr->n_pairs;
+    P.n_entries = reinterpret_cast<unsigned long long*>(&hdr->n_entries);
     prep_kernel<<<div_up(FN, 128), 128, 0, s>>>(P);
     count_launch();
     if (int rc = check_launch("prep_kernel")) return rc;
   }
-  // K2 scan of per-primitive tile counts -> entry offsets, total -> header
-  if (int rc = scan_exclusive(counts, offs, FN, scan_tmp, &hdr->n_entries, s)) return rc;
+  // K2 scan of per-primitive tile counts -> entry offsets.  The entry total
+  // in the header is prep's 64-bit sum: the int32 scan may wrap for batches
+  // past 2^31 entries, and the check below rejects those before emit reads
+  // the offsets.
+  if (int rc = scan_exclusive(counts, offs, FN, scan_tmp, nullptr, s)) return rc;
   if (prof) cudaEventRecord(g_prof.ev[pset][1], s);
   header_out_kernel<<<1, 1, 0, s>>>(hdr, hmap);
   count_launch();
@@ -329,8 +333,9 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     return set_error(SQV_ERR_INVALID_PRIM, "primitive %lld failed validation (bits %d)",
                      (long long)(h.bad_word >> 8), (int)(h.bad_word & 255u));
   }
-  const int64_t E = h.n_entries;
-  if (E >= (1LL << 31) - 1) return set_error(SQV_ERR_ARG, "too many bin entries (split frames)");
+  const int64_t E = h.n_entries;  // exact (64-bit atomics in prep)
+  if (E < 0 || E >= (1LL << 31) - 1)
+    return set_error(SQV_ERR_ARG, "too many bin entries: %lld (split frames)", (long long)E);
   L = layout(FN, FT, lrow, E);
   if (ws_needed) *ws_needed = L.total;
   if (ws_bytes < L.total)

@@ -19,6 +19,9 @@ struct PrepArgs {
   int* windows;  // [FN][6]
   unsigned long long* bad_word;
   unsigned long long* n_pairs;
+  // 64-bit sum of counts[]: the (tile, primitive) entry total, checked on the
+  // host before the 32-bit scan offsets and emit are trusted
+  unsigned long long* n_entries;
 };
 
 struct EmitArgs {
@@ -73,7 +76,8 @@ __global__ void tile_bounds_kernel(const uint32_t* keys, int64_t n, int64_t n_ti
 
 // exclusive scan of n int32 values; out has n+1 entries (out[n] = total);
 // if total64 != nullptr the total is also stored there.  tmp needs
-// scan_tmp_ints(n) ints.
+// scan_tmp_ints(n) ints.  The running sums are int32: callers bound the
+// total below 2^31 first (sqv_voxelize checks prep's 64-bit entry total).
 int64_t scan_tmp_ints(int64_t n);
 int scan_exclusive(const int* in, int* out, int64_t n, int* tmp, long long* total64,
                    cudaStream_t s);

@@ -171,11 +171,21 @@ __global__ void prep_kernel(PrepArgs A) {
   const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t FN = (int64_t)A.n_frames * A.n_prims;
   unsigned long long v = gi < FN ? (unsigned long long)prep_prim(A, gi) : 0ull;
-  // one atomic per warp for the algorithmic pair count (not one per primitive
-  // on a single address)
+  // the entry total in 64 bits (counts[gi] was just written by this thread):
+  // the int32 scan that follows wraps past 2^31 entries, so the host checks
+  // this sum, not the scan's, before emit trusts the offsets
+  unsigned long long e = gi < FN ? (unsigned long long)A.counts[gi] : 0ull;
+  // one atomic per warp for each total (not one per primitive on a single
+  // address)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(A.n_pairs, v);
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_down_sync(0xffffffffu, v, o);
+    e += __shfl_down_sync(0xffffffffu, e, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (v) atomicAdd(A.n_pairs, v);
+    if (e) atomicAdd(A.n_entries, e);
+  }
 }
 
 // K3: one thread per primitive; entries in (tz, ty, tx) order, primitive

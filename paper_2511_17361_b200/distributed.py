@@ -49,16 +49,36 @@ def evaluate_stream(voxelizer, batches, gt_labels, n_classes: int, group=None):
     return allreduce_confusion(cm, group)
 
 
+def gt_jitter_device(gt_seed: int, first_frame: int, n_frames: int, n_prims: int,
+                     n_classes: int, device=None):
+    """Per-frame N(0, 1) jitter draws for the ground-truth copy of frames
+    first_frame .. first_frame+n_frames-1: (d_mu [F, N, 3], d_logits [F, N, C]).
+
+    They come from the same counter-based Philox stream as the scenes
+    (``sqv_gen_frames`` keyed by gt_seed: its C + 3 standard normals per
+    primitive, the first 3 for mu, the rest for the logits), so the draws of
+    a frame depend only on (gt_seed, frame, primitive): never on the batch
+    size or the rank's shard.  The confusion counts are therefore identical
+    for any frames_per_batch and any GPU count."""
+    from .scenegen import gen_frames_device
+    z = gen_frames_device(gt_seed, n_frames, n_prims, n_classes + 3,
+                          first_frame=first_frame, device=device).logits
+    return z[..., :3], z[..., 3:]
+
+
 def evaluate_generated(voxelizer, seed: int, n_frames: int, n_prims: int,
                        frames_per_batch: int = 100, gt_seed: int | None = None,
                        sigma_mu: float = 0.2, sigma_logit: float = 0.5, smin: float = 0.2,
-                       smax: float = 4.0, emin: float = 0.2, group=None):
+                       smax: float = 4.0, emin: float = 0.2, group=None,
+                       frame_range: tuple[int, int] | None = None):
     """The config-5 stream with no host in the loop: this rank's frame shard
     is generated in HBM (``scenegen.gen_frames_device``: frame f depends only
     on (seed, f), so shards need no coordination), the ground truth is a
-    jittered copy (mu + N(0, sigma_mu), logits + N(0, sigma_logit), device
-    RNG seeded per batch), both are voxelized and their confusion counts
-    accumulated, then all-reduced once.  Returns the global counts."""
+    jittered copy (mu + N(0, sigma_mu), logits + N(0, sigma_logit), drawn
+    per frame by ``gt_jitter_device``), both are voxelized and their
+    confusion counts accumulated, then all-reduced once.  Returns the global
+    counts, bit-identical for any frames_per_batch and world size.
+    ``frame_range`` overrides this rank's shard (default ``shard_frames``)."""
     import torch
     import torch.distributed as dist
     from .core import PrimitiveBatch
@@ -74,20 +94,15 @@ def evaluate_generated(voxelizer, seed: int, n_frames: int, n_prims: int,
     gt_seed = seed + 1 if gt_seed is None else gt_seed
     K = C + 1
     cm = torch.zeros((K, K), dtype=torch.int64, device=dev)
-    start, stop = shard_frames(n_frames, rank, world)
+    start, stop = frame_range if frame_range is not None else shard_frames(n_frames, rank, world)
     for f0 in range(start, stop, frames_per_batch):
         F = min(frames_per_batch, stop - f0)
         b = gen_frames_device(seed, F, n_prims, C, origin=spec.origin, dims=spec.dims,
                               resolution=spec.resolution, smin=smin, smax=smax, emin=emin,
                               first_frame=f0, device=dev)
-        g = torch.Generator(device=dev)
-        g.manual_seed(int(gt_seed) * 1000003 + f0)
-        gt = PrimitiveBatch(b.mu + sigma_mu * torch.randn(b.mu.shape, generator=g, device=dev,
-                                                          dtype=torch.float64),
-                            b.scale, b.rot, b.opacity, b.eps,
-                            b.logits + sigma_logit * torch.randn(b.logits.shape, generator=g,
-                                                                 device=dev,
-                                                                 dtype=torch.float64))
+        d_mu, d_lg = gt_jitter_device(gt_seed, f0, F, n_prims, C, device=dev)
+        gt = PrimitiveBatch(b.mu + sigma_mu * d_mu, b.scale, b.rot, b.opacity, b.eps,
+                            b.logits + sigma_logit * d_lg)
         pred_l = voxelizer(b, dense=False).labels
         gt_l = voxelizer(gt, dense=False).labels
         confusion_matrix(pred_l, gt_l, C, out=cm)

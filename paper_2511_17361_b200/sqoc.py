@@ -40,23 +40,34 @@ class SqocGrid:
     v_o: np.ndarray | None = None  # float32, same shape
 
 
-def _x_fastest(a: np.ndarray, dims) -> np.ndarray:
-    """Accept (nz, ny, nx) memory-order arrays or logical (nx, ny, nz) views."""
+def _x_fastest(a: np.ndarray, dims, logical: bool) -> np.ndarray:
+    """x-fastest memory order (nz, ny, nx) of ``a``.
+
+    ``logical=False``: ``a`` already is the memory-order array (nz, ny, nx)
+    (or any array with that C-order element sequence).  ``logical=True``: ``a``
+    is the SPEC's logical (nx, ny, nz) view (``SemanticGrid.labels``,
+    ``DenseGrids.v_o``) and is transposed.  The layout is never inferred from
+    the shape: for nx == nz both layouts have the same shape."""
     nx, ny, nz = dims
-    if a.shape == (nx, ny, nz) and (nx, ny, nz) != (nz, ny, nx):
+    if logical:
+        if a.shape != (nx, ny, nz):
+            raise ValueError(f"logical grid must have shape {(nx, ny, nz)}, got {a.shape}")
         a = a.transpose(2, 1, 0)
+    elif a.size != nx * ny * nz:
+        raise ValueError(f"grid has {a.size} voxels, dims {(nx, ny, nz)} need {nx * ny * nz}")
     return np.ascontiguousarray(a.reshape(nz, ny, nx))
 
 
 def write(path: str, dims, origin, resolution: float, n_classes: int, labels,
-          free_index: int | None = None, v_o=None) -> None:
+          free_index: int | None = None, v_o=None, *, logical: bool = False) -> None:
     """Write a grid.  ``labels`` uses ``free_index`` (default C) for free
-    voxels; it is stored as 255."""
+    voxels; it is stored as 255.  ``labels`` / ``v_o`` are memory-order
+    (nz, ny, nx) arrays, or logical (nx, ny, nz) views with ``logical=True``."""
     nx, ny, nz = (int(d) for d in dims)
     if n_classes < 1 or n_classes > 255:
         raise ValueError("SQOC stores 1..255 classes")
     free = n_classes if free_index is None else int(free_index)
-    lab = _x_fastest(np.asarray(labels), (nx, ny, nz)).astype(np.int64)
+    lab = _x_fastest(np.asarray(labels), (nx, ny, nz), logical).astype(np.int64)
     if np.any(((lab < 0) | (lab >= n_classes)) & (lab != free)):
         raise ValueError("labels outside [0, C) that are not the free index")
     lab = np.where(lab == free, FREE, lab).astype(np.uint8)
@@ -66,7 +77,7 @@ def write(path: str, dims, origin, resolution: float, n_classes: int, labels,
     if v_o is None:
         body.append(b"\x00")
     else:
-        vo = _x_fastest(np.asarray(v_o, dtype=np.float32), (nx, ny, nz)).astype("<f4")
+        vo = _x_fastest(np.asarray(v_o, dtype=np.float32), (nx, ny, nz), logical).astype("<f4")
         body += [b"\x01", vo.tobytes()]
     d = os.path.dirname(os.path.abspath(path))
     fd, tmp = tempfile.mkstemp(dir=d, prefix=".sqoc.")
@@ -108,6 +119,8 @@ def read(path: str) -> SqocGrid:
 
 
 def write_semantic_grid(path: str, sem, dense=None) -> None:
-    """Write a SemanticGrid (+ optional DenseGrids.v_o) from voxelize()."""
+    """Write a SemanticGrid (+ optional DenseGrids.v_o) from voxelize(): both
+    hold the SPEC's logical (nx, ny, nz) views."""
     write(path, sem.spec.dims, sem.spec.origin, sem.spec.resolution, len(sem.classes),
-          sem.labels, sem.classes.free_index, None if dense is None else dense.v_o)
+          sem.labels, sem.classes.free_index, None if dense is None else dense.v_o,
+          logical=True)

@@ -104,10 +104,13 @@ class VoxelizeConfig:
 
 @dataclass
 class DenseGrids:
-    """v_o (nx, ny, nz) >= 0 and v_c (nx, ny, nz, C) (SPEC.md:328-331)."""
+    """v_o (nx, ny, nz) >= 0 and v_c (nx, ny, nz, C) (SPEC.md:328-331).
+    ``spec`` (optional) is the grid the arrays were voxelized on; voxelize()
+    sets it and finalize() carries it into the SemanticGrid."""
 
     v_o: Any
     v_c: Any
+    spec: Any = None
 
 
 @dataclass
@@ -430,7 +433,8 @@ def _run_scene(scene, spec, cfg, truncate):
     v_o = r.v_o[0].cpu().numpy()
     v_c = r.v_c[0].cpu().numpy()
     lab = labels_to_host(lab, r.free_code, classes.free_index)
-    return (SemanticGrid(_logical(lab), spec, classes), DenseGrids(_logical(v_o), _logical(v_c)))
+    return (SemanticGrid(_logical(lab), spec, classes),
+            DenseGrids(_logical(v_o), _logical(v_c), spec))
 
 
 def voxelize(scene, spec: VoxelGridSpec = VoxelGridSpec(),
@@ -446,8 +450,14 @@ def voxelize_bruteforce(scene, spec: VoxelGridSpec = VoxelGridSpec(),
     return _run_scene(scene, spec, cfg, truncate=False)
 
 
-def finalize(dense: DenseGrids, tau: float, classes: ClassTable) -> SemanticGrid:
-    """Labels from dense grids — the device finalize kernel."""
+def finalize(dense: DenseGrids, tau: float, classes: ClassTable,
+             spec: VoxelGridSpec | None = None) -> SemanticGrid:
+    """Labels from dense grids — the device finalize kernel.
+
+    The SemanticGrid's geometry (it feeds ray_iou and the SQOC header) is
+    ``spec``, else ``dense.spec`` (set by voxelize), else the Occ3D default
+    when the dims match it; any other grid needs one of the two, and
+    finalize raises rather than attach the default origin/resolution to it."""
     import torch
     dev = _lib.require_cuda()
     L = _lib.lib()
@@ -469,8 +479,20 @@ def finalize(dense: DenseGrids, tau: float, classes: ClassTable) -> SemanticGrid
     _lib.check(L.sqv_finalize(t_vo.data_ptr(), t_vc.data_ptr(), vo_mem.size, C, float(tau), code,
                               lab.data_ptr(), _lib.stream_ptr(dev)), "sqv_finalize")
     lab_h = labels_to_host(lab.cpu().numpy(), code, classes.free_index)
-    spec = VoxelGridSpec(dims=shape)
-    return SemanticGrid(_logical(lab_h), spec, classes)
+    return SemanticGrid(_logical(lab_h), _grid_spec_for(shape, spec, dense), classes)
+
+
+def _grid_spec_for(shape, spec, dense) -> VoxelGridSpec:
+    spec = spec if spec is not None else getattr(dense, "spec", None)
+    if spec is None:
+        if tuple(shape) != VoxelGridSpec().dims:
+            raise ValueError(f"dense grids of dims {tuple(shape)} carry no grid geometry: "
+                             "pass spec= (the default Occ3D origin/resolution only "
+                             "applies to 200x200x16)")
+        return VoxelGridSpec()
+    if tuple(spec.dims) != tuple(shape):
+        raise ValueError(f"spec dims {spec.dims} differ from the dense grids' {tuple(shape)}")
+    return spec
 
 
 def truncation_report(batch: PrimitiveBatch, spec: VoxelGridSpec = VoxelGridSpec(),

@@ -44,12 +44,32 @@ def test_device_generator_matches_mirror_and_voxelizes():
 
 
 @pytest.mark.gpu
-def test_evaluate_generated_shards_sum_to_whole():
+def test_evaluate_generated_independent_of_batching_and_shards():
+    """The ground-truth jitter is keyed per frame, so the full confusion
+    matrix is identical for any frames_per_batch, and shard matrices sum to
+    the whole (what the NCCL all-reduce computes for any GPU count)."""
     from paper_2511_17361_b200 import distributed as D
     vox = P.Voxelizer(P.VoxelGridSpec(), P.VoxelizeConfig(), 18)
     whole = D.evaluate_generated(vox, 5, 6, 400, frames_per_batch=6).cpu().numpy()
-    parts = D.evaluate_generated(vox, 5, 6, 400, frames_per_batch=2).cpu().numpy()
-    np.testing.assert_array_equal(whole.sum(), 6 * 640000)
-    # batching changes only the jitter draws, not the predicted frames: the
-    # prediction marginal (column sums) is identical
-    np.testing.assert_array_equal(whole.sum(0), parts.sum(0))
+    assert whole.sum() == 6 * 640000
+    for fpb in (1, 2, 4):
+        other = D.evaluate_generated(vox, 5, 6, 400, frames_per_batch=fpb).cpu().numpy()
+        np.testing.assert_array_equal(whole, other, err_msg=f"frames_per_batch={fpb}")
+    for world in (2, 4):
+        parts = sum(D.evaluate_generated(vox, 5, 6, 400, frames_per_batch=3,
+                                         frame_range=D.shard_frames(6, r, world)).cpu().numpy()
+                    for r in range(world))
+        np.testing.assert_array_equal(whole, parts, err_msg=f"world={world}")
+    # the jitter is a real perturbation: gt differs from the prediction
+    assert np.trace(whole) < whole.sum()
+
+
+@pytest.mark.gpu
+def test_gt_jitter_keyed_per_frame():
+    from paper_2511_17361_b200.distributed import gt_jitter_device
+    a_mu, a_lg = gt_jitter_device(11, 0, 5, 300, 18)
+    b_mu, b_lg = gt_jitter_device(11, 3, 2, 300, 18)
+    np.testing.assert_array_equal(a_mu[3:].cpu().numpy(), b_mu.cpu().numpy())
+    np.testing.assert_array_equal(a_lg[3:].cpu().numpy(), b_lg.cpu().numpy())
+    assert a_mu.shape == (5, 300, 3) and a_lg.shape == (5, 300, 18)
+    assert abs(float(a_lg.std()) - 1.0) < 0.05

@@ -261,6 +261,13 @@ def test_dropin_scene_api_and_spec_examples():
     occ = [int(np.sum(P.finalize(dense, t, classes).labels != classes.free_index))
            for t in (0.005, 0.01, 0.02)]
     assert occ[0] >= occ[1] >= occ[2]
+    # finalize keeps the grid geometry: from dense.spec, or spec=; a bare
+    # non-default DenseGrids is rejected rather than given the Occ3D origin
+    assert P.finalize(dense, 0.01, classes).spec == spec
+    bare = P.DenseGrids(dense.v_o, dense.v_c)
+    with pytest.raises(ValueError, match="spec="):
+        P.finalize(bare, 0.01, classes)
+    np.testing.assert_array_equal(P.finalize(bare, 0.01, classes, spec=spec).labels, sem.labels)
 
 
 def test_sigma_scaling_argmax_invariance():
@@ -543,4 +550,53 @@ def test_block_cull_bound_with_large_logits(scale):
     out = _run(b, spec, cfg, 18)
     ref, _ = _oracle(b, spec, cfg, out["free_code"])
     assert out["n_pairs"] == ref["n_pairs"]
-    assert_parity(out, ref, cfg.tau, out["free_code"], min_agreement=0.0)
+    # tau = 0 labels every voxel; voxels whose whole oracle v_o is below the
+    # cull's drop bound may lose every contribution (v_c = 0 -> label 0):
+    # allowed by the near-tie rule (gap < 2 * 2e-12), and excluded from the
+    # agreement rate, which must still reach 99.99% on the rest
+    _, lab = assert_parity(out, ref, cfg.tau, out["free_code"])
+    assert lab["n_resolvable"] > 0.5 * out["labels"].size
+
+
+def test_entry_total_past_2_31_reports_split_frames():
+    """The bin entry total is summed in 64 bits by prep: a batch
+    past 2^31 entries fails with the 'split frames' error before the int32
+    scan offsets reach emit — not a wrapped total (a bogus workspace size,
+    or out-of-bounds emit stores).  5,000 untruncated primitives on a
+    4096x4096x16 grid (262,144 tiles per frame) x 2 frames = 2.6e9 entries;
+    only prep and the scan run, so the call is cheap."""
+    import ctypes
+    import torch
+    P = _pkg()
+    from paper_2511_17361_b200 import _lib
+    from paper_2511_17361_b200.scenegen import gen_frames_device
+    spec = P.VoxelGridSpec((-40.0, -40.0, -1.0), (4096, 4096, 16), 0.4)
+    b = gen_frames_device(3, 2, 5000, 4, origin=spec.origin, dims=spec.dims,
+                          resolution=spec.resolution)
+    L = _lib.lib()
+    Pr = _lib.Prims()
+    Pr.mu, Pr.scale, Pr.rot = b.mu.data_ptr(), b.scale.data_ptr(), b.rot.data_ptr()
+    Pr.opacity, Pr.eps, Pr.logits = b.opacity.data_ptr(), b.eps.data_ptr(), b.logits.data_ptr()
+    Pr.n_valid = None
+    Pr.n_frames, Pr.n_prims, Pr.n_classes = 2, 5000, 4
+    cfg = _lib.Cfg()
+    cfg.tau, cfg.neighborhood_radius, cfg.truncate = 0.01, 5, 0
+    cfg.semantic_mode, cfg.free_label, cfg.window_extent, cfg.precision = 0, 255, 2.5, 1
+    grid = spec._c()
+    dummy = torch.empty(16, dtype=torch.uint8, device="cuda")
+    O_ = _lib.Outputs()
+    O_.labels = dummy.data_ptr()
+    fixed = int(L.sqv_workspace_bytes(2, 5000, 4, ctypes.byref(grid), 0))
+    ws = torch.empty(fixed, dtype=torch.uint8, device="cuda")
+    need = ctypes.c_size_t(0)
+    bp, bb = ctypes.c_int64(0), ctypes.c_int32(0)
+    rc = L.sqv_voxelize(ctypes.byref(Pr), ctypes.byref(grid), ctypes.byref(cfg),
+                        ctypes.byref(O_), None, ws.data_ptr(), ws.numel(), ctypes.byref(need),
+                        ctypes.byref(bp), ctypes.byref(bb), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    msg = _lib.last_error()
+    assert rc == _lib.SQV_ERR_ARG, (rc, msg)
+    assert "split frames" in msg, msg
+    E = int(re.search(r"entries: (\d+)", msg).group(1))
+    tiles = 512 * 512
+    assert E == 2 * 5000 * tiles  # untruncated: every primitive overlaps every tile
