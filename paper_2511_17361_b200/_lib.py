@@ -10,7 +10,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libsqv.so")
+# SQV_LIB: an alternative build of the same library (A/B runs of compile-time
+# variants, scripts/gpu_ab_env.sh); the default is the in-tree build
+LIB_PATH = os.environ.get("SQV_LIB") or os.path.join(_HERE, "_build", "libsqv.so")
 
 SQV_OK = 0
 SQV_ERR_ARG = -1

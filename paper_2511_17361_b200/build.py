@@ -18,7 +18,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OUT = os.path.join(PKG, "_build")
+OUT = os.environ.get("SQV_BUILD_DIR") or os.path.join(PKG, "_build")  # variant builds: A/B only
 LIB = os.path.join(OUT, "libsqv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",

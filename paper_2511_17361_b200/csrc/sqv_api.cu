@@ -99,7 +99,7 @@ Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
   L.keys_b = take((size_t)n_entries * 4);
   L.vals_b = take((size_t)n_entries * 4);
   L.radix_tmp = take((size_t)radix_tmp_ints(n_entries) * 4);
-  L.bmask = take((size_t)n_entries * 2);
+  L.bmask = take((size_t)n_entries * 4);
   L.total = o;
   return L;
 }
@@ -389,7 +389,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
                                                          &hdr->deep_count);
   count_launch();
   if (int rc = check_launch("tile_bounds_kernel")) return rc;
-  uint16_t* bmask = (uint16_t*)(ws + L.bmask);
+  uint32_t* bmask = (uint32_t*)(ws + L.bmask);
 
   // K5 evaluate + finalize
   EvalArgs A;
@@ -425,7 +425,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     A.bmask = bmask;
     if (!ffma && E > 0)
       if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, lrows, lrow, tile_off,
-                                      (int)T, ntx, nty, N, bmask, s))
+                                      (int)T, ntx, nty, N,
+                                      cfg->precision ? SQV_ACC_C : INFINITY, bmask, s))
         return rc;
     A.tc_max_entries = ffma ? -1 : depth;
     A.ffma_min_entries = ffma ? -1 : depth;

@@ -40,6 +40,11 @@ constexpr float kFCut = 87.3365f;
 constexpr double kBlockCutMin = SQV_BLOCK_CUT;
 constexpr double kLnInvDropBound = 26.937873;  // ln(1 / 2e-12)
 constexpr float kLog2e = 1.4426950408889634f;
+// Strict mode's accurate-log threshold: primitives with 2/eps1 = c above it
+// take FMA-pipe logs (their exponent amplifies the MUFU lg2 error).
+#ifndef SQV_ACC_C
+#define SQV_ACC_C 4.0f
+#endif
 
 constexpr int kTileX = SQV_TILE_X, kTileY = SQV_TILE_Y, kTileZ = SQV_TILE_Z;
 

@@ -47,12 +47,14 @@ namespace {
 // conservative); the shared parts are computed once per entry (local block
 // centres differ by fixed lattice steps), and a block whose nearest local
 // corner is deep inside — (2^b + 1) max|x'|^c well below the primitive's cut
-// — is marked without the 8-MUFU field test.  A "hit" that could have been
+// — is marked without the 8-MUFU field test.  Bit 16 flags strict mode's
+// accurate-log primitives (c > acc_c), so the evaluator's list build needs
+// only the mask.  A "hit" that could have been
 // culled only costs evaluation work: those pairs get their exact FP32 w.
 __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t n,
                                    const float* recs, const float* lrows, int lrow,
                                    const int* tile_off, int tiles_per_frame, int ntx, int nty,
-                                   int n_prims, uint16_t* bmask) {
+                                   int n_prims, float acc_c, uint32_t* bmask) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const uint32_t key = keys[e];
@@ -129,7 +131,9 @@ __global__ void block_masks_kernel(const uint32_t* keys, const int* ids, int64_t
     }
     if (hit) m |= (1u << bb) | ((unsigned)(ix[ox] && iy[oy] && iz[oz]) << (8 + bb));
   }
-  bmask[e] = (uint16_t)m;
+  // strict mode: the evaluator's accurate-log list (FMA-pipe logs for c > acc_c)
+  if (m && R.c > acc_c) m |= 1u << 16;
+  bmask[e] = m;
 }
 
 }  // namespace
@@ -138,12 +142,12 @@ bool eval_tc_supported(int cm) { return cm <= 24; }
 
 int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
                        const float* recs, const float* lrows, int lrow, const int* tile_off,
-                       int tiles_per_frame, int ntx, int nty, int n_prims, uint16_t* bmask,
-                       cudaStream_t s) {
+                       int tiles_per_frame, int ntx, int nty, int n_prims, float acc_c,
+                       uint32_t* bmask, cudaStream_t s) {
   if (n_entries <= 0) return SQV_OK;
   block_masks_kernel<<<(unsigned)((n_entries + 127) / 128), 128, 0, s>>>(
       sorted_keys, sorted_ids, n_entries, recs, lrows, lrow, tile_off, tiles_per_frame, ntx, nty,
-      n_prims, bmask);
+      n_prims, acc_c, bmask);
   count_launch();
   return check_launch("block_masks_kernel");
 }

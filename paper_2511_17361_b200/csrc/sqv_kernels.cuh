@@ -58,15 +58,17 @@ struct EvalArgs {
   const int* deep_count;  // their number (device)
   int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
   int64_t n_entries;  // (tile, primitive) entries of the batch
-  const uint16_t* bmask;  // per entry: bit b = may hit warp block b, bit 8+b = covers it
+  // per entry: bit b = may hit warp block b, bit 8+b = covers it, bit 16 =
+  // strict mode's accurate-log primitive (c > SQV_ACC_C)
+  const uint32_t* bmask;
 };
 
 // per (tile, primitive) entry: the 8 warp-block tests of the tensor-core
 // evaluator (block_may_hit / block_inside), computed once, in parallel
 int block_masks_launch(const uint32_t* sorted_keys, const int* sorted_ids, int64_t n_entries,
                        const float* recs, const float* lrows, int lrow, const int* tile_off,
-                       int tiles_per_frame, int ntx, int nty, int n_prims, uint16_t* bmask,
-                       cudaStream_t s);
+                       int tiles_per_frame, int ntx, int nty, int n_prims, float acc_c,
+                       uint32_t* bmask, cudaStream_t s);
 
 __global__ void prep_kernel(PrepArgs A);
 __global__ void emit_kernel(EmitArgs A);

@@ -421,12 +421,16 @@ def test_degenerate_inputs_and_free_index():
 
 
 @pytest.mark.parametrize("n_prims", [256, 2000])
-def test_persistent_and_per_tile_evaluators_bit_identical(monkeypatch, n_prims):
-    """The persistent evaluator (tile counter, prefetch under the epilogue)
-    and one CTA per tile run the same per-tile code: identical bits."""
+@pytest.mark.parametrize("stream", ["0", "1"])
+def test_persistent_and_per_tile_evaluators_bit_identical(monkeypatch, n_prims, stream):
+    """The persistent evaluator (work counter) and one CTA per work item run
+    the same per-tile code: identical bits, for the chunk-staged kernel
+    (SQV_STREAM=0, the default for sparse batches) and the streaming one
+    (SQV_STREAM=1, the default for dense batches)."""
     P = _pkg()
     from paper_2511_17361_b200.scenegen import gen_frames
     spec = P.VoxelGridSpec()
+    monkeypatch.setenv("SQV_STREAM", stream)
     for prec in ("strict", "fast"):
         cfg = P.VoxelizeConfig(precision=prec)
         b = gen_frames(31, 3, n_prims)
@@ -466,11 +470,15 @@ def test_randomized_configurations(case):
                smax=float(rng.choice([1.0, 4.0])))
     nv = rng.integers(0, N + 1, F).astype(np.int32)
     b = PrimitiveBatch(b.mu, b.scale, b.rot, b.opacity, b.eps, b.logits, n_valid=nv)
+    # all four evaluator variants: persistent or per work item, chunk-staged
+    # or streaming
     os.environ["SQV_PERSIST"] = str(case % 2)
+    os.environ["SQV_STREAM"] = str((case // 2) % 2)
     try:
         out = _run(b, spec, cfg, C, truncate=truncate, bins=True)
     finally:
         del os.environ["SQV_PERSIST"]
+        del os.environ["SQV_STREAM"]
     ref, grid = _oracle(b, spec, cfg, out["free_code"], truncate=truncate)
     np.testing.assert_array_equal(out["windows"], ref["windows"])
     off, ids = O.bins(ref["windows"], grid.dims)
@@ -520,11 +528,13 @@ def test_randomized_dense_configurations(case):
     cfg = P.VoxelizeConfig(semantic_mode=mode, precision=prec)
     b = _scene(9000 + case, N, C, frames=2, origin=origin, dims=dims, resolution=res,
                emin=float(rng.choice([0.1, 0.2])))
-    os.environ["SQV_PERSIST"] = str(case % 2)  # deep tiles in both evaluator modes
+    os.environ["SQV_PERSIST"] = str(case % 2)  # deep tiles in every evaluator variant
+    os.environ["SQV_STREAM"] = str((case // 2) % 2)
     try:
         out = _run(b, spec, cfg, C, bins=True)
     finally:
         del os.environ["SQV_PERSIST"]
+        del os.environ["SQV_STREAM"]
     ref, grid = _oracle(b, spec, cfg, out["free_code"])
     off, ids = O.bins(ref["windows"], grid.dims)
     np.testing.assert_array_equal(out["tile_off"], off)
