@@ -271,8 +271,11 @@ def run_ours(a, rank, world, local_rank):
     outs = [out, vox.alloc(B, dense=True)]
     pairs_box = [0]
 
+    entries_box = [0]
+
     def conf(k, r):
         pairs_box[0] += r.n_pairs
+        entries_box[0] += r.n_entries
         confusion_matrix(r.labels, gt[k % n_batches], C, out=cm)
 
     # ---- warm-up ----
@@ -285,6 +288,7 @@ def run_ours(a, rank, world, local_rank):
     _lib.profile_read(reset=True)
     n_launch0 = _lib.launch_count()
     pairs = 0
+    entries_box[0] = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -328,6 +332,18 @@ def run_ours(a, rank, world, local_rank):
                 "algorithmic": f"2 x {C + 1} FLOP per in-window pair (class sums + sigma)",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32)" if pk else None}
 
+    def evaluator_name(entries_per_tile):
+        # the library's choice (sqv_eval_tc_impl.cuh launch_tc): dense batches
+        # stream, sparse ones (< 64 entries per tile) run the chunk-staged
+        # persistent kernel; SQV_EVAL / SQV_STREAM override it (A/B runs)
+        if os.environ.get("SQV_EVAL") == "ffma":
+            return "eval_kernel (FFMA, sqv_eval.cu)"
+        st = os.environ.get("SQV_STREAM")
+        stream = entries_per_tile >= 64 if st is None else st != "0"
+        return ("eval_tcs_kernel (tcgen05, per-warp streaming, 4 warps per CTA; "
+                "sqv_eval_tc_impl.cuh)" if stream else
+                "eval_tc_kernel (tcgen05, chunk-staged; sqv_eval_tc_impl.cuh)")
+
     # roofline of the dominant kernel (eval_kernel): algorithmic MUFU ops per
     # launch / its CUDA-event duration inside the timed region
     eval_s = prof["eval_ms"] * 1e-3 / max(prof["calls"], 1)
@@ -353,8 +369,7 @@ def run_ours(a, rank, world, local_rank):
                 "unit": "Gop/s (MUFU ex2/lg2)", "frac": achieved / mufu_peak, "traffic": traffic,
                 "traffic_source": traffic_src, "sfu_busy_ncu": sfu_busy,
                 "algorithmic_bytes_per_launch": B * spec.n_voxels * (1 + 4 + 4 * C),
-                "kernel": "eval_tc_kernel (tcgen05, sqv_eval_tc_impl.cuh)" if os.environ.get(
-                    "SQV_EVAL") != "ffma" else "eval_kernel (FFMA, sqv_eval.cu)",
+                "kernel": evaluator_name(entries_box[0] / max(K * B * vox.tiles_per_frame, 1)),
                 "algorithmic": f"{MUFU_PER_PAIR} MUFU per in-window (primitive, voxel) pair x "
                                f"{pairs_per_launch:.4e} pairs per launch",
                 "eval_ms_per_launch": eval_s * 1e3,

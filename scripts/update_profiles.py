@@ -3,7 +3,7 @@ profiles/<tag>_*: bench lines, config sweep, launch list + summary, ncu
 metrics of the evaluator.  usage: update_profiles.py TAG"""
 import json, os, shutil, subprocess, sys
 
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 G, P = "gpurun_out", "profiles"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.chdir(ROOT)
@@ -34,7 +34,7 @@ for line in summ.splitlines():
     parts = line.split()
     if len(parts) == 2 and "__" in parts[0]:
         m[parts[0]] = float(parts[1])
-json.dump({"kernel": "eval_tc_kernel<18, 6> (strict)", "frames_per_launch": 10,
+json.dump({"kernel": "eval_tcs_kernel<18, 6, false, 4> (strict, streaming)", "frames_per_launch": 10,
            "dram_bytes_read": m.get("dram__bytes_read.sum", 0) * 1e6,
            "dram_bytes_write": m.get("dram__bytes_write.sum", 0) * 1e6,
            "duration_ms_under_ncu": m.get("gpu__time_duration.sum"),
