@@ -94,12 +94,6 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 #ifndef SQV_EXP_POLY
 #define SQV_EXP_POLY 0
 #endif
-#ifndef SQV_ZLOG_POLY
-#define SQV_ZLOG_POLY 0
-#endif
-#ifndef SQV_DIAG
-#define SQV_DIAG 0
-#endif
 
 // log2_acc on a pair: the exponent split is integer work per lane, the
 // polynomial runs packed.
@@ -261,9 +255,8 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
     const float2 uy = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
     // fast mode folds log2(log2 e) into the exponents (2^(u + k) = log2(e)
     // 2^u; see stage_exps); strict keeps the separate scaling
-    // SQV_ZLOG_POLY (A/B): the z log on the FMA pipe for every primitive
-    const float2 lz = (ACC || SQV_ZLOG_POLY) ? log2_acc2(abs2(cd.P[2][h])) : log2p<false>(cd.P[2][h]);
-    float2 uz = EXACT_STEP ? mul2(bc2(c), lz) : fma2(bc2(c), lz, bc2(kLog2Log2e));
+    float2 uz = EXACT_STEP ? mul2(bc2(c), log2p<ACC>(cd.P[2][h]))
+                           : fma2(bc2(c), log2p<ACC>(cd.P[2][h]), bc2(kLog2Log2e));
     // umin - umax = -|ux - uy| (the same rounded value); both coordinates 0
     // give NaN, clamped to -126 (t ~ 0) while umax = -inf makes S^b = 0
     S.um[h] = make_float2(fmaxf(ux.x, uy.x), fmaxf(ux.y, uy.y));
@@ -272,9 +265,7 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
     // fast mode takes one voxel pair's t on the FMA pipe (+1.4%: the SFU
     // binds there; strict, whose accurate logs load the FMA pipe, is neutral
     // with it and -1.1% with both pairs' t there, so it keeps the SFU)
-    if (SQV_DIAG == 2)  // diagnostics only (wrong results): t without the SFU
-      S.t[h] = d;
-    else if (SQV_EXP_POLY >= 2 || (!EXACT_STEP && h == 0))
+    if (SQV_EXP_POLY >= 2 || (!EXACT_STEP && h == 0))
       S.t[h] = ex2_poly2(d);
     else
       S.t[h] = make_float2(ex2(d.x), ex2(d.y));
@@ -303,11 +294,7 @@ template <bool FOLD>
 __device__ __forceinline__ void stage_exps(const PairState& S, float (&w)[kVPT]) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-#if SQV_DIAG == 1  // diagnostics only (wrong results): no log2(1+t) polynomial
-    const float2 l1p = S.t[h];
-#else
     const float2 l1p = log2_1p_poly2(S.t[h]);
-#endif
     float2 F, arg;
     if (FOLD) {
       const float2 e = fma2(bc2(S.b), add2(S.um[h], l1p), bc2(kLog2Log2e));
