@@ -901,7 +901,10 @@ int launch_tc(const EvalArgs& A, int n_tiles, int field, cudaStream_t s) {
   // 12% slower, its per-warp list build and first copies sit in the L2
   // latency of every small tile).  SQV_STREAM=0/1 forces either (A/B).
   int mode = pipelined && !persist ? 4 : 0;
+  // (two work items per bin tile: keep the item index in int range)
+  const bool stream_ok = n_tiles < (1 << 30);
   if (const char* se = std::getenv("SQV_STREAM")) mode = pipelined && std::atoi(se) != 0 ? 4 : 0;
+  if (!stream_ok) mode = 0;
   void (*kern)(EvalArgs);
   int smem_bytes, threads, ctas_per_sm, items;
   if (mode == 4) {
