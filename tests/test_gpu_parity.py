@@ -610,3 +610,32 @@ def test_entry_total_past_2_31_reports_split_frames():
     E = int(re.search(r"entries: (\d+)", msg).group(1))
     tiles = 512 * 512
     assert E == 2 * 5000 * tiles  # untruncated: every primitive overlaps every tile
+
+
+def test_torch_ops_match_the_package_api():
+    """torch.ops.sqocc.voxelize / prep_bin / confusion give the bits of
+    Voxelizer and confusion_matrix, and pass torch.library.opcheck's schema
+    and fake-tensor checks."""
+    import torch
+    P = _pkg()
+    from paper_2511_17361_b200 import torch_ops  # noqa: F401
+    from paper_2511_17361_b200.metrics import confusion_matrix
+    from paper_2511_17361_b200.scenegen import gen_frames
+    spec = P.VoxelGridSpec((-10.0, -9.0, -1.0), (52, 44, 20), 0.4)
+    b = gen_frames(77, 2, 300, 12, origin=spec.origin, dims=spec.dims, resolution=spec.resolution)
+    vox = P.Voxelizer(spec, P.VoxelizeConfig(), 12)
+    db = vox.to_device(b)
+    args = (db.mu, db.scale, db.rot, db.opacity, db.eps, db.logits, list(spec.origin),
+            list(spec.dims), spec.resolution)
+    lab, vo, vc = torch.ops.sqocc.voxelize(*args)
+    r = vox(db, dense=True, bins=True)
+    for x, y in ((lab, r.labels), (vo, r.v_o), (vc, r.v_c)):
+        assert torch.equal(x, y)
+    w, to, ids, n = torch.ops.sqocc.prep_bin(*args)
+    assert torch.equal(w, r.bins["windows"]) and torch.equal(to, r.bins["tile_off"])
+    assert torch.equal(ids, r.bins["prim_ids"]) and int(n) == r.n_pairs
+    gt = torch.roll(lab, 1, dims=-1).contiguous()
+    assert torch.equal(torch.ops.sqocc.confusion(lab, gt, 12), confusion_matrix(lab, gt, 12))
+    utils = ("test_schema", "test_faketensor")
+    torch.library.opcheck(torch.ops.sqocc.voxelize.default, args, test_utils=utils)
+    torch.library.opcheck(torch.ops.sqocc.confusion.default, (lab, gt, 12), test_utils=utils)

@@ -180,3 +180,31 @@ def test_confusion_allreduce_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     np.testing.assert_array_equal(got, want)
+
+
+def test_torch_ops_registered_with_fake_shapes():
+    """torch.ops.sqocc.{voxelize, prep_bin, confusion}: schemas
+    and fake (meta) shapes on CPU; the real kernels need CUDA (no fallback)."""
+    import torch
+    from paper_2511_17361_b200 import torch_ops  # noqa: F401
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    from torch.fx.experimental.symbolic_shapes import ShapeEnv
+    F, N, C = 2, 5, 18
+    m = lambda *s: torch.empty(s, dtype=torch.float64, device="meta")  # noqa: E731
+    lab, vo, vc = torch.ops.sqocc.voxelize(m(F, N, 3), m(F, N, 3), m(F, N, 4), m(F, N), m(F, N, 2),
+                                          m(F, N, C), [-40.0, -40.0, -1.0], [200, 200, 16], 0.4)
+    assert lab.shape == (F, 16, 200, 200) and lab.dtype == torch.uint8
+    assert vo.shape == (F, 16, 200, 200) and vc.shape == (F, 16, 200, 200, C)
+    u8 = torch.empty(10, dtype=torch.uint8, device="meta")
+    cm = torch.ops.sqocc.confusion(u8, u8, C)
+    assert cm.shape == (C + 1, C + 1) and cm.dtype == torch.int64
+    with FakeTensorMode(shape_env=ShapeEnv()):
+        f = lambda *s: torch.empty(s, dtype=torch.float64)  # noqa: E731
+        w, to, ids, n = torch.ops.sqocc.prep_bin(f(F, N, 3), f(F, N, 3), f(F, N, 4), f(F, N),
+                                                 f(F, N, 2), f(F, N, C), [-40.0, -40.0, -1.0],
+                                                 [200, 200, 16], 0.4)
+        assert w.shape == (F, N, 6) and to.shape == (F * 625 + 1,) and n.shape == ()
+    z = lambda *s: torch.zeros(s, dtype=torch.float64)  # noqa: E731
+    with pytest.raises(RuntimeError):
+        torch.ops.sqocc.voxelize(z(F, N, 3), z(F, N, 3), z(F, N, 4), z(F, N), z(F, N, 2),
+                                 z(F, N, C), [-40.0, -40.0, -1.0], [200, 200, 16], 0.4)
