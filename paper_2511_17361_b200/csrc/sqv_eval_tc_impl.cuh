@@ -144,6 +144,20 @@ __device__ __forceinline__ void tile_epilogue(const EvalArgs& A, uint8_t* smem, 
   const bool lab8 = full && (nx & 7) == 0 && (V & 7) == 0 &&
                     (reinterpret_cast<uintptr_t>(A.labels) & 7) == 0;
   if (vc_bulk && vo_bulk && lab8) {
+    // v_c rows (8*C floats) as bulk copies, one per (row, layer) lane; the
+    // 32-byte v_o rows as two 16-byte lane stores each (all 32 lanes), the
+    // 8-byte label rows as one lane store each
+    {
+      const int p = lane >> 1, half = lane & 1;
+      const int ry = RPW * warp + p / LZ, zl = p % LZ;
+      const int yy = y_t + ry;
+      if (A.v_o && zl < zend && yy < ny) {
+        const int64_t gv =
+            (int64_t)f * V + (int64_t)x_t + (int64_t)nx * (yy + (int64_t)ny * (z_t + zl));
+        *reinterpret_cast<float4*>(A.v_o + gv + half * 4) =
+            *reinterpret_cast<const float4*>(s_vo + zl * zpo + ry * kTileX + half * 4);
+      }
+    }
     const int ry = RPW * warp + lane / LZ, zl = lane % LZ;
     const int yy = y_t + ry;
     if (lane < 16 && zl < zend && yy < ny) {
@@ -151,9 +165,6 @@ __device__ __forceinline__ void tile_epilogue(const EvalArgs& A, uint8_t* smem, 
       if (A.v_c)
         tc::bulk_store(A.v_c + gv * C, tc::smem_u32(s_vc + zl * zpc + ry * kTileX * C),
                        (uint32_t)(kTileX * C * 4));
-      if (A.v_o)
-        tc::bulk_store(A.v_o + gv, tc::smem_u32(s_vo + zl * zpo + ry * kTileX),
-                       (uint32_t)(kTileX * 4));
       *reinterpret_cast<uint2*>(A.labels + gv) =
           *reinterpret_cast<const uint2*>(s_lab + zl * zpo + ry * kTileX);
     }
