@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           auto step = [&](int off, PairState& nxt, const PairState& cur, float(&w)[kVPT]) {
             const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + off);
             nxt.cw = class_weight(off);
-            stage_exps<FIELD == 7>(cur, w);
+            stage_exps<true>(cur, w);
             stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
           };
           PairState s0, s1;
@@ -459,10 +459,10 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
           if (k < cnt) {
             step(off, s1, s0, w);
             push(w, s0.cw);
-            stage_exps<FIELD == 7>(s1, w);
+            stage_exps<true>(s1, w);
             push(w, s1.cw);
           } else {
-            stage_exps<FIELD == 7>(s0, w);
+            stage_exps<true>(s0, w);
             push(w, s0.cw);
           }
         };
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
             PairState st;
             float w[kVPT];
             stage_logs<true, true, true>(R, x, y, z0, st);  // exact steps, window test, acc logs
-            stage_exps<FIELD == 7>(st, w);
+            stage_exps<true>(st, w);
             push(w, class_weight(off));
           }
       } else {
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
           const uint8_t* rec = slot(q);
           const PrimRec& R = *reinterpret_cast<const PrimRec*>(rec);
           nxt.cw = class_weight(rec);
-          stage_exps<FIELD == 7>(cur, w);
+          stage_exps<true>(cur, w);
           stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, nxt);
         };
         PairState s0, s1;
@@ -838,10 +838,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
           feed(base + k, base + k);
           step(base + k, s1, s0, w);
           push(w, s0.cw);
-          stage_exps<FIELD == 7>(s1, w);
+          stage_exps<true>(s1, w);
           push(w, s1.cw);
         } else {
-          stage_exps<FIELD == 7>(s0, w);
+          stage_exps<true>(s0, w);
           push(w, s0.cw);
         }
       };
@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
           PairState st;
           float w[kVPT];
           stage_logs<true, true, true>(*reinterpret_cast<const PrimRec*>(rec), x, y, z0, st);
-          stage_exps<FIELD == 7>(st, w);
+          stage_exps<true>(st, w);
           push(w, class_weight(rec));
         }
       __syncwarp();  // every slot read before the next segment refills the ring

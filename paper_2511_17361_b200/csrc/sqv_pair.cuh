@@ -253,10 +253,9 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
   for (int h = 0; h < 2; ++h) {
     const float2 ux = mul2(bc2(a), log2p<ACC>(cd.P[0][h]));
     const float2 uy = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
-    // fast mode folds log2(log2 e) into the exponents (2^(u + k) = log2(e)
-    // 2^u; see stage_exps); strict keeps the separate scaling
-    float2 uz = EXACT_STEP ? mul2(bc2(c), log2p<ACC>(cd.P[2][h]))
-                           : fma2(bc2(c), log2p<ACC>(cd.P[2][h]), bc2(kLog2Log2e));
+    // log2(log2 e) folded into the exponents (2^(u + k) = log2(e) 2^u; see
+    // stage_exps)
+    float2 uz = fma2(bc2(c), log2p<ACC>(cd.P[2][h]), bc2(kLog2Log2e));
     // umin - umax = -|ux - uy| (the same rounded value); both coordinates 0
     // give NaN, clamped to -126 (t ~ 0) while umax = -inf makes S^b = 0
     S.um[h] = make_float2(fmaxf(ux.x, uy.x), fmaxf(ux.y, uy.y));
@@ -286,10 +285,11 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
 // Stage 2: log2(1 + t), S^b, Z, F and w = exp(-F).  w = 0 exactly once
 // -F log2(e) < -126 (ftz), i.e. for every F > kFCut — the same zero the block
 // cull assumes — so no select is needed (F is never NaN: see above).
-// FOLD (fast mode, paired with stage_logs<false, ..>): the exponents carry
+// FOLD (paired with stage_logs, which folds k into uz): the exponents carry
 // k = log2(log2 e), so F log2(e) = 2^(e + k) + 2^(uz + k) needs no scaling
-// multiply (fast: +0.7% and max |dv_o|/v_o 1.1e-5 -> 1.0e-5; strict measured
-// -0.9% with it and keeps the multiply).
+// multiply (fast: +0.7% and max |dv_o|/v_o 1.1e-5 -> 1.0e-5; strict: -0.9%
+// in the round-1 chunk-staged kernel, +0.7% config 2 / +0.6% config 3 in
+// the streaming one, worst config-1 |dv_o|/v_o 9.0e-6 -> 7.6e-6).
 template <bool FOLD>
 __device__ __forceinline__ void stage_exps(const PairState& S, float (&w)[kVPT]) {
 #pragma unroll
@@ -350,7 +350,7 @@ __device__ __forceinline__ void pair_weights(const PrimRec& R, int x, int y, int
       stage_logs<FIELD == 6, LIVE, true>(R, x, y, z0, S);
     else
       stage_logs<FIELD == 6, LIVE, false>(R, x, y, z0, S);
-    stage_exps<FIELD == 7>(S, w);
+    stage_exps<true>(S, w);
     return;
   }
   ColCoords2 cd;
