@@ -383,11 +383,11 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
       }
       __syncwarp();
       // the operands are single-buffered: a K step's MMAs must complete
-      // before the next primitive's stores.  Strict mode waits right before
-      // those stores (the next primitive's field overlaps the MMAs: +0.8%),
-      // fast mode right after the issue (the other placement measured 2%
-      // slower there; code layout)
-      constexpr bool kLateWait = FIELD == 6;
+      // before the next primitive's stores.  Both modes wait right after the
+      // issue (round 1 had strict wait right before the next stores, +0.8%
+      // then; with the folded exponents of round 2 the early wait is +0.6%
+      // on config 1)
+      constexpr bool kLateWait = false;
       auto push = [&](const float(&w)[kVPT], float cw) {
         if (kLateWait) wait_free();
         store_k(kk, w, cw);
