@@ -34,7 +34,8 @@ from torch import Tensor
 from .voxelize import (PRECISIONS, SEMANTIC_MODES, VoxelGridSpec, VoxelizeConfig, Voxelizer,
                        free_code_for)
 
-_VOXELIZERS: dict = {}
+_VOXELIZERS: dict = {}  # (grid, config, C, free index, device) -> Voxelizer (its workspaces)
+_MAX_CACHED = 16
 
 
 def _voxelizer(origin, dims, resolution, tau, radius, mode, precision, truncate, C, free_index,
@@ -52,6 +53,8 @@ def _voxelizer(origin, dims, resolution, tau, radius, mode, precision, truncate,
                              precision=precision)
         v = Voxelizer(spec, cfg, C, None if free_index < 0 else free_index, truncate=truncate,
                       device=device)
+        if len(_VOXELIZERS) >= _MAX_CACHED:  # bounded: drop the oldest configuration
+            _VOXELIZERS.pop(next(iter(_VOXELIZERS)))
         _VOXELIZERS[key] = v
     return v
 
