@@ -100,12 +100,21 @@ __device__ __forceinline__ void tile_epilogue(const EvalArgs& A, uint8_t* smem, 
     const int loc = vx + kTileX * vy;  // within the z layer
     int best = 0;
     float bv = vals[0];
+    if (C == CM) {  // the usual case: no per-class bound test
 #pragma unroll
-    for (int k = 1; k < CM; ++k)
-      if (k < C && vals[k] > bv) {
-        bv = vals[k];
-        best = k;
-      }
+      for (int k = 1; k < CM; ++k)
+        if (vals[k] > bv) {
+          bv = vals[k];
+          best = k;
+        }
+    } else {
+#pragma unroll
+      for (int k = 1; k < CM; ++k)
+        if (k < C && vals[k] > bv) {
+          bv = vals[k];
+          best = k;
+        }
+    }
     const float vo = vals[CM];
     if (A.v_c) {
       if ((CM & 1) == 0 && C == CM) {  // 8-byte stores: zpc and loc * C are even
