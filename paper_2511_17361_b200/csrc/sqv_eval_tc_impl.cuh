@@ -23,37 +23,43 @@ constexpr int kN = 32;       // class weights + sigma, padded
 constexpr int kTmemCols = kWarps * kN;  // 256 -> two CTAs per SM fill the 512 columns
 constexpr uint32_t kIdesc = tc::idesc_tf32(128, kN, 1, 1);
 
-template <int CM>
+template <int CM, int NW = 8>
 struct TcShape {
   static_assert(CM + 1 <= kN, "sigma column must fit in N");
+  static_assert(NW == 8 || NW == 4, "8 or 4 warp blocks per CTA");
   static constexpr int kLRow = (CM + 1 + 3) & ~3;
 #ifdef SQV_CHUNK
-  static constexpr int kChunk = CM <= 18 ? SQV_CHUNK : 104;
+  static constexpr int kChunk8 = CM <= 18 ? SQV_CHUNK : 104;
 #else
-  static constexpr int kChunk = CM <= 18 ? 120 : 104;
+  static constexpr int kChunk8 = CM <= 18 ? 120 : 104;
 #endif
+  // 4-warp CTAs (four per SM; one z half of a bin tile) stage at most
+  // 2 x 128 threads / 2 = 64 primitives per chunk and fit 4 x 55 KB of shared
+  // memory with 48.  (Measured for sparse batches, config 1: fast +6.4%,
+  // strict -0.6% against 8 warps; not instantiated.)
+  static constexpr int kChunk = NW == 8 ? kChunk8 : (CM <= 18 ? 48 : 40);
   // operand buffers (1 KB aligned): per warp A_hi, A_lo (4 KB each), B_hi, B_lo (1 KB each)
   static constexpr int kA = 0;
-  static constexpr int kB = kA + kWarps * 2 * 4096;
+  static constexpr int kB = kA + NW * 2 * 4096;
   // staged primitives: record (40 words) + class weights/sigma (kLRow) each
   static constexpr int kStride = kRecWords + kLRow;  // words
-  static constexpr int kRec = kB + kWarps * 2 * 1024;
+  static constexpr int kRec = kB + NW * 2 * 1024;
   // per-warp hit lists (offsets of staged primitives in 16 B units): primitives
   // whose window covers the warp's whole block from the front, the rest from
   // the back
   static constexpr int kList = kRec + kChunk * kStride * 4;
   static_assert(kStride % 4 == 0, "16-byte aligned staging");
-  static constexpr int kBm = kList + kWarps * kChunk * 2;  // staged block masks (u16)
+  static constexpr int kBm = kList + NW * kChunk * 2;  // staged block masks (u16)
   static constexpr int kAcc = kBm + kChunk * 2;  // strict: per-warp u8 lists of accurate-log primitives
-  static constexpr int kBar = (kAcc + kWarps * kChunk + 7) & ~7;
-  static constexpr int kMisc = kBar + kWarps * 8;   // tmem base (4 B) + has flags (8 x 4 B)
-  static constexpr int kEnd = kMisc + 4 + kWarps * 4 + 4;  // + next-tile slot
+  static constexpr int kBar = (kAcc + NW * kChunk + 7) & ~7;
+  static constexpr int kMisc = kBar + NW * 8;   // tmem base (4 B) + has flags (NW x 4 B)
+  static constexpr int kEnd = kMisc + 4 + NW * 4 + 4;  // + next-tile slot
   // epilogue staging (aliases kA..): z layers padded by 8 words so the 4 lanes
   // holding z-adjacent voxels hit different banks
-  static constexpr int kStage = 16 * ((64 * CM + 8) * 4 + 72 * 4 + 72);
+  static constexpr int kStage = 2 * NW * ((64 * CM + 8) * 4 + 72 * 4 + 72);
   static constexpr int kBody = kEnd > kStage ? kEnd : kStage;
   static constexpr int kSmem = kBody + 1024;               // + alignment slack
-  static_assert(kSmem <= 113 * 1024, "two CTAs per SM");
+  static_assert((16 / NW) * (kSmem + 1024) <= 228 * 1024, "CTAs per SM by shared memory");
   static_assert(kStage <= kMisc, "staging must not overwrite the flags");
 };
 
@@ -213,9 +219,11 @@ __device__ __forceinline__ void tile_epilogue(const EvalArgs& A, uint8_t* smem, 
   }
 }
 
-template <int CM, int FIELD, bool PERSIST>
-__global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
-  using S = TcShape<CM>;
+template <int CM, int FIELD, bool PERSIST, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tc_kernel(EvalArgs A) {
+  using S = TcShape<CM, NW>;
+  constexpr int kHalves = 8 / NW;  // CTAs per bin tile (NW = 4: one per z half)
+  const int n_items = A.n_tiles * kHalves;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* s_rec = smem + S::kRec;
@@ -226,9 +234,12 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + S::kMisc);
   int* s_has = reinterpret_cast<int*>(smem + S::kMisc + 4);
 
-  int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + kWarps * 4);
-  if (!PERSIST && A.tile_off[blockIdx.x + 1] - A.tile_off[blockIdx.x] > A.tc_max_entries)
-    return;  // a deep tile: the CUDA-core evaluator (launched next) owns it
+  int* s_next = reinterpret_cast<int*>(smem + S::kMisc + 4 + NW * 4);
+  if (!PERSIST) {
+    const int tg = (int)blockIdx.x / kHalves;
+    if (A.tile_off[tg + 1] - A.tile_off[tg] > A.tc_max_entries)
+      return;  // a deep tile: the CUDA-core evaluator (launched next) owns it
+  }
   // warp index and TMEM base through a lane-0 shuffle: provably warp-uniform
   // for ptxas, so the MMA operands derived from them live in uniform
   // registers (no per-issue elect/broadcast loops)
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
 
   // ---- TMEM + barriers ----
   if (warp == 0) {
-    tc::tmem_alloc(s_tmem, kTmemCols);
+    tc::tmem_alloc(s_tmem, NW * kN);
     tc::tmem_relinquish();
   }
   if (lane == 0) tc::mbar_init(&s_bar[warp], 1);
@@ -319,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
   constexpr bool kSplitAcc = FIELD == 6;
   auto stage_chunk = [&](int64_t fb, int c0, int n) {
     // two threads per primitive, every 16-byte piece in flight at once
-    static_assert(2 * S::kChunk <= kThreads, "staging map");
+    static_assert(2 * S::kChunk <= NW * 32, "staging map");
     const int j = tid >> 1;
     if (j < n) {
       if ((tid & 1) == 0) s_bm[j] = (uint16_t)A.bmask[c0 + j];
@@ -332,17 +343,19 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         tc::cp_async16(dst + q * 16, q < kRecWords / 4 ? rsrc + q : lsrc + (q - kRecWords / 4));
     }
   };
-  int tile_g = blockIdx.x;
+  int item = blockIdx.x;
   bool prefetched = false;
-  while (tile_g < A.n_tiles) {
+  while (item < n_items) {
+    const int tile_g = item / kHalves, half = item - tile_g * kHalves;
+    const int blk = half * NW + warp;  // this warp's block of the bin tile (mask bit)
     const int f = tile_g / A.tiles_per_frame;
     const int t = tile_g - f * A.tiles_per_frame;
     const int tx = t % A.ntx;
     const int ty = (t / A.ntx) % A.nty;
     const int tz = t / (A.ntx * A.nty);
-    const int bx0 = tx * kTileX + (warp & 1) * 4;
-    const int by0 = ty * kTileY + ((warp >> 1) & 1) * 4;
-    const int bz0 = tz * kTileZ + (warp >> 2) * 8;
+    const int bx0 = tx * kTileX + (blk & 1) * 4;
+    const int by0 = ty * kTileY + ((blk >> 1) & 1) * 4;
+    const int bz0 = tz * kTileZ + (blk >> 2) * 8;
     const int x = bx0 + (lane & 3);
     const int y = by0 + ((lane >> 2) & 3);
     const int z0 = bz0 + (lane >> 4) * 4;
@@ -372,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
         const int j = q * 32 + lane;
         // this warp's bits of the precomputed block masks (block_masks_kernel)
         const unsigned m = j < n ? (unsigned)s_bm[j] : 0u;
-        bool hit = (m >> warp) & 1u, inside = (m >> (8 + warp)) & 1u;
+        bool hit = (m >> blk) & 1u, inside = (m >> (8 + blk)) & 1u;
         if (kSplitAcc) {  // strict: accurate-log primitives get their own list
           const bool acc =
               hit && reinterpret_cast<const PrimRec*>(s_rec + j * S::kStride * 4)->c > SQV_ACC_C;
@@ -512,29 +525,30 @@ __global__ void __launch_bounds__(kThreads, 2) eval_tc_kernel(EvalArgs A) {
     tc::fence_before_sync();
     __syncthreads();  // all MMAs complete; operand smem is free for staging
     tc::fence_after_sync();
-    const int next_tile = PERSIST ? *s_next : A.n_tiles;
+    const int next_item = PERSIST ? *s_next : n_items;
     prefetched = false;
-    if (PERSIST && kPrefetch && next_tile < A.n_tiles) {
-      const int nb = A.tile_off[next_tile], ne = A.tile_off[next_tile + 1];
+    if (PERSIST && kPrefetch && next_item < n_items) {
+      const int ntg = next_item / kHalves;
+      const int nb = A.tile_off[ntg], ne = A.tile_off[ntg + 1];
       if (ne > nb && ne - nb <= A.tc_max_entries) {
-        const int nf = next_tile / A.tiles_per_frame;
+        const int nf = ntg / A.tiles_per_frame;
         stage_chunk((int64_t)nf * A.n_prims, nb, min(S::kChunk, ne - nb));
         prefetched = true;
       }
     }
 
-    tile_epilogue<CM>(A, smem, s_has, tmem_base, warp, lane, f, tx, ty, tz);
+    tile_epilogue<CM, NW>(A, smem, s_has, tmem_base, warp, lane, f, tx, ty, tz, half * 8);
 
     // all TMEM reads and bulk-copy reads of the staging are done before the
-    // next tile's MMAs and operand stores reuse them
-    if (PERSIST && next_tile < A.n_tiles) {
+    // next item's MMAs and operand stores reuse them
+    if (PERSIST && next_item < n_items) {
       tc::fence_before_sync();
       __syncthreads();
       tc::fence_after_sync();
     }
-    tile_g = next_tile;
-  }  // tile loop
-  if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
+    item = next_item;
+  }  // item loop
+  if (warp == 0) tc::tmem_dealloc(tmem_base, NW * kN);
 }
 
 
