@@ -221,6 +221,14 @@ int sqv_gen_frames(uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t
 int sqv_profile_enable(int on);
 int sqv_profile_read(double* ms, int64_t* calls, int reset);
 
+/* Evaluator work counters: while attached, every sqv_voxelize call adds to
+ * counters[0] the MUFU (SFU) operations its evaluators issue (thread level)
+ * and to counters[1] the (primitive, voxel) pairs they evaluate (whole warp
+ * blocks of 128 voxels, so culled-in but window-dead voxels count).  The
+ * caller owns the int64[2] device buffer; NULL detaches.  One atomic pair per
+ * warp and staged chunk; for benchmarks, not part of the reference API. */
+int sqv_stats_attach(int64_t* counters);
+
 /* Microbenchmarks of the pipes that bound the evaluator (roofline
  * denominators measured on the running GPU): which = 0 -> MUFU (SFU) ex2/lg2
  * ops/s, 1 -> FP32 FFMA lanes/s.  *ops_per_s receives the achieved rate. */

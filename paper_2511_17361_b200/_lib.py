@@ -93,13 +93,14 @@ def lib():
     L.sqv_profile_enable.argtypes = [ctypes.c_int]
     L.sqv_profile_read.argtypes = [_c_p, ctypes.POINTER(_i64), ctypes.c_int]
     L.sqv_microbench.argtypes = [ctypes.c_int, ctypes.POINTER(_f64), _c_p]
+    L.sqv_stats_attach.argtypes = [_c_p]
     L.sqv_ray_iou.argtypes = [_c_p, _c_p, _i32, ctypes.POINTER(Grid), _i32, _c_p, _c_p, _i64,
                               _c_p, _i32, _c_p, ctypes.POINTER(RayHits), _c_p]
     L.sqv_gen_frames.argtypes = [ctypes.c_uint64, _i64, _i32, _i32, _i32, ctypes.POINTER(Grid),
                                  _f64, _f64, _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]
     for f in ("sqv_voxelize", "sqv_finalize", "sqv_confusion", "sqv_density",
               "sqv_profile_enable", "sqv_profile_read", "sqv_microbench", "sqv_ray_iou",
-              "sqv_gen_frames"):
+              "sqv_gen_frames", "sqv_stats_attach"):
         getattr(L, f).restype = ctypes.c_int
     if L.sqv_abi_version() != 1:
         raise RuntimeError("libsqv ABI version mismatch")
@@ -110,7 +111,7 @@ def lib():
 EXPORTED = ("sqv_abi_version", "sqv_last_error", "sqv_launch_count", "sqv_tiles_per_frame",
             "sqv_workspace_bytes", "sqv_voxelize", "sqv_finalize", "sqv_confusion",
             "sqv_density", "sqv_profile_enable", "sqv_profile_read", "sqv_microbench",
-            "sqv_ray_iou", "sqv_gen_frames")
+            "sqv_ray_iou", "sqv_gen_frames", "sqv_stats_attach")
 
 
 def last_error() -> str:
@@ -160,3 +161,10 @@ def microbench(which: int) -> float:
     v = _f64(0.0)
     check(lib().sqv_microbench(int(which), ctypes.byref(v), stream_ptr()), "sqv_microbench")
     return float(v.value)
+
+
+def stats_attach(counters) -> None:
+    """Attach an int64[2] device tensor as the evaluator work counters
+    (include/sqv.h sqv_stats_attach); None detaches."""
+    check(lib().sqv_stats_attach(None if counters is None else counters.data_ptr()),
+          "sqv_stats_attach")

@@ -13,6 +13,7 @@
 namespace sqv {
 
 static std::atomic<long long> g_launches{0};
+static std::atomic<unsigned long long*> g_stats{nullptr};  // sqv_stats_attach
 static thread_local char g_err[512] = "";
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -420,6 +421,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   A.deep_tiles = deep;
   A.deep_count = &hdr->deep_count;
   A.n_entries = E;
+  A.stats = g_stats.load();
   if (prof) cudaEventRecord(g_prof.ev[pset][3], s);
   {
     A.bmask = bmask;
@@ -562,6 +564,11 @@ int sqv_gen_frames(uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t
   A.eps = eps;
   A.logits = logits;
   return gen_launch(A, (cudaStream_t)stream);
+}
+
+int sqv_stats_attach(int64_t* counters) {
+  g_stats.store(reinterpret_cast<unsigned long long*>(counters));
+  return SQV_OK;
 }
 
 int sqv_profile_enable(int on) {

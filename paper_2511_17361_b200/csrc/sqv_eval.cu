@@ -114,12 +114,15 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
     }
     __syncwarp();
 
+    unsigned long long st_mufu = 0, st_blocks = 0;  // instrumentation (A.stats)
     for (int q = 0; q * 32 < n; ++q) {
       unsigned m = s_mask[warp * kMaskWords + q];
       while (m) {
         const int j = q * 32 + __ffs(m) - 1;
         m &= m - 1;
         const PrimRec& R = *reinterpret_cast<const PrimRec*>(s_rec + j * kRecWords);
+        st_mufu += mufu_per_block(FIELD, wants_acc<FIELD>(R));
+        ++st_blocks;
         float w[kVPT];
         pair_weights<FIELD>(R, x, y, z0, w);
         const float4* lw = reinterpret_cast<const float4*>(s_lw + j * S::kLRow);
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, (CM <= 18 ? 2 : 1)) eval_kernel(Eval
         }
       }
     }
+    if (lane == 0) add_stats(A.stats, st_mufu, st_blocks);
   }
 
   // ---- epilogue: finalize + staged coalesced stores ----------------------

@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tc_kernel(EvalArgs A) {
         n_part += __popc(mp);
       }
       __syncwarp();
+      if (lane == 0)
+        add_stats(A.stats, (n_in + n_part) * mufu_per_block(FIELD, false) +
+                               n_acc * mufu_per_block(FIELD, true), n_in + n_part + n_acc);
       // the operands are single-buffered: a K step's MMAs must complete
       // before the next primitive's stores.  Both modes wait right after the
       // issue (round 1 had strict wait right before the next stores, +0.8%
@@ -771,6 +774,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
       // right before its first item is read, and batch b+1 is issued once
       // batch b-1 has been read (its half of the ring is free) ----
       const int n_seq = n_in + n_part + n_acc;
+      if (lane == 0)
+        add_stats(A.stats, (n_in + n_part) * mufu_per_block(FIELD, false) +
+                               n_acc * mufu_per_block(FIELD, true), n_seq);
       constexpr int kH = S::kD / 2;           // items per batch
       int issued = 0;                          // batches issued
       auto copy_batch = [&](int bt) {

@@ -58,6 +58,10 @@ struct EvalArgs {
   const int* deep_count;  // their number (device)
   int* tile_counter;  // zeroed device int: the persistent evaluator's work counter
   int64_t n_entries;  // (tile, primitive) entries of the batch
+  // optional instrumentation (sqv_stats_attach): [0] += MUFU ops issued by
+  // the evaluators (thread level), [1] += evaluated (primitive, voxel) pairs
+  // (warp blocks run x 128, window-dead voxels of partial blocks included)
+  unsigned long long* stats;
   // per entry: bit b = may hit warp block b, bit 8+b = covers it, bit 16 =
   // strict mode's accurate-log primitive (c > SQV_ACC_C)
   const uint32_t* bmask;
@@ -89,6 +93,21 @@ int scan_exclusive(const int* in, int* out, int64_t n, int* tmp, long long* tota
 int64_t radix_tmp_ints(int64_t n);
 int radix_sort(uint32_t* keys, int* vals, uint32_t* keys_alt, int* vals_alt, int64_t n, int bits,
                int* tmp, int* which, cudaStream_t s);
+
+// MUFU ops per evaluated voxel of each field form, times 128 voxels per warp
+// block: strict 7 (3 lg2 + 4 ex2), strict accurate-log 4 (ex2 only), fast 6.5
+// (one voxel pair's t on the FMA pipe), the 8- and 9-MUFU diagnostic forms
+__host__ __device__ constexpr unsigned long long mufu_per_block(int field, bool acc) {
+  return field == 6 ? (acc ? 512ull : 896ull)
+                    : field == 7 ? 832ull : field == 8 ? 1024ull : 1152ull;
+}
+__device__ __forceinline__ void add_stats(unsigned long long* st, unsigned long long mufu,
+                                          unsigned long long blocks) {
+  if (st) {
+    atomicAdd(st, mufu);
+    atomicAdd(st + 1, blocks * 128ull);
+  }
+}
 
 // evaluator
 int eval_cm_for(int C);  // padded class count for C (0 if unsupported)

@@ -639,3 +639,29 @@ def test_torch_ops_match_the_package_api():
     utils = ("test_schema", "test_faketensor")
     torch.library.opcheck(torch.ops.sqocc.voxelize.default, args, test_utils=utils)
     torch.library.opcheck(torch.ops.sqocc.confusion.default, (lab, gt, 12), test_utils=utils)
+
+
+def test_evaluator_work_counters():
+    """sqv_stats_attach: MUFU ops and evaluated pairs of the evaluators, whole
+    128-voxel warp blocks, between 4 and 7 MUFU per evaluated pair (strict),
+    fewer evaluated pairs than the window pairs they were culled from."""
+    import torch
+    P = _pkg()
+    from paper_2511_17361_b200 import _lib
+    from paper_2511_17361_b200.scenegen import gen_frames
+    vox = P.Voxelizer(P.VoxelGridSpec(), P.VoxelizeConfig(), 18)
+    b = vox.to_device(gen_frames(4, 2, 2000, 18))
+    st = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.stats_attach(st)
+    try:
+        r = vox(b, dense=False)
+        torch.cuda.synchronize()
+    finally:
+        _lib.stats_attach(None)
+    mufu, pairs = (int(v) for v in st.cpu().tolist())
+    assert pairs > 0 and pairs % 128 == 0
+    assert 4 * pairs <= mufu <= 7 * pairs
+    assert 0.5 * r.n_pairs < pairs < r.n_pairs
+    vox(b, dense=False)  # detached: counters unchanged
+    torch.cuda.synchronize()
+    assert int(st[0]) == mufu
