@@ -93,7 +93,11 @@ __device__ __forceinline__ void tile_epilogue(const EvalArgs& A, uint8_t* smem, 
     const int mb = (NW == 8 ? (warp & 4) : 0) + i;  // M block (= producing warp)
     float vals[32];
     if (s_has[mb]) {
-      tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN), vals);
+      const uint32_t ta = tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(mb * kN);
+      if (CM + 1 <= 20)
+        tc::tmem_ld_32x32b_x20(ta, vals);  // classes + sigma only
+      else
+        tc::tmem_ld_32x32b_x32(ta, vals);
     } else {
 #pragma unroll
       for (int k = 0; k < 32; ++k) vals[k] = 0.0f;
