@@ -215,9 +215,10 @@ int sqv_gen_frames(uint64_t seed, int64_t first_frame, int32_t n_frames, int32_t
  * When enabled, sqv_voxelize records CUDA events around its device stages on
  * the caller's stream and accumulates their durations:
  *   ms[0] prep + count scan, ms[1] emit + radix sort + tile scan,
- *   ms[2] evaluate + finalize (the hot kernel), ms[3] sum of the three.
+ *   ms[2] block masks + evaluate + finalize, ms[3] sum of the three,
+ *   ms[4] evaluate + finalize alone (the hot kernel).
  * sqv_profile_read synchronises the pending events; reset != 0 zeroes. */
-#define SQV_NSTAGES 4
+#define SQV_NSTAGES 5
 int sqv_profile_enable(int on);
 int sqv_profile_read(double* ms, int64_t* calls, int reset);
 

@@ -148,12 +148,12 @@ def profile_enable(on: bool = True) -> None:
 def profile_read(reset: bool = False) -> dict:
     """Accumulated stage device times (ms) of sqv_voxelize calls since the last reset."""
     import numpy as np
-    ms = np.zeros(4, np.float64)
+    ms = np.zeros(5, np.float64)
     calls = _i64(0)
     check(lib().sqv_profile_read(ms.ctypes.data_as(_c_p), ctypes.byref(calls), int(reset)),
           "sqv_profile_read")
     return {"prep_scan_ms": ms[0], "bin_sort_ms": ms[1], "eval_ms": ms[2], "total_ms": ms[3],
-            "calls": int(calls.value)}
+            "eval_kernel_ms": ms[4], "calls": int(calls.value)}
 
 
 def microbench(which: int) -> float:

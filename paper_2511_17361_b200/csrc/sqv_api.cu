@@ -144,10 +144,10 @@ struct Profiler {
   std::mutex mu;
   bool on = false;
   bool created = false;
-  cudaEvent_t ev[kRing][5];
+  cudaEvent_t ev[kRing][6];
   bool pending[kRing] = {};
   int next = 0;
-  double ms[SQV_NSTAGES] = {0, 0, 0, 0};
+  double ms[SQV_NSTAGES] = {0, 0, 0, 0, 0};
   long long calls = 0;
   void ensure() {
     if (!created) {
@@ -163,11 +163,12 @@ struct Profiler {
   }
   void fold(int i) {
     const double m0 = el(ev[i][0], ev[i][1]), m1 = el(ev[i][2], ev[i][3]),
-                 m2 = el(ev[i][3], ev[i][4]);
+                 m2 = el(ev[i][3], ev[i][4]), m4 = el(ev[i][5], ev[i][4]);
     ms[0] += m0;
     ms[1] += m1;
     ms[2] += m2;
     ms[3] += m0 + m1 + m2;
+    ms[4] += m4;
     calls++;
     pending[i] = false;
   }
@@ -430,6 +431,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
                                       (int)T, ntx, nty, N,
                                       cfg->precision ? SQV_ACC_C : INFINITY, bmask, s))
         return rc;
+    if (prof) cudaEventRecord(g_prof.ev[pset][5], s);
     A.tc_max_entries = ffma ? -1 : depth;
     A.ffma_min_entries = ffma ? -1 : depth;
     if (ffma) {
