@@ -71,12 +71,12 @@ static Header* mapped_header() {
 }
 
 struct Layout {
-  size_t hdr, recs, lrows, counts, offs, windows, tile_off, deep, scan_tmp;  // fixed
+  size_t hdr, recs, lrows, counts, offs, windows, tile_off, deep, scan_tmp, frame_count;  // fixed
   size_t keys_a, vals_a, keys_b, vals_b, radix_tmp, bmask;                       // variable
   size_t fixed_end, total;
 };
 
-Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
+Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries, int64_t F = 0) {
   Layout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -94,6 +94,7 @@ Layout layout(int64_t FN, int64_t FT, int lrow, int64_t n_entries) {
   L.deep = take((size_t)FT * 4);
   const int64_t st = scan_tmp_ints(FN > FT ? FN : FT);
   L.scan_tmp = take((size_t)st * 4);
+  L.frame_count = take((size_t)(F + 1) * 4);
   L.fixed_end = o;
   L.keys_a = take((size_t)n_entries * 4);
   L.vals_a = take((size_t)n_entries * 4);
@@ -222,7 +223,7 @@ size_t sqv_workspace_bytes(int32_t n_frames, int32_t n_prims, int32_t n_classes,
   if (!cm) return 0;
   const int lrow = (cm + 1 + 3) & ~3;
   const int64_t T = sqv_tiles_per_frame(grid);
-  return layout((int64_t)n_frames * n_prims, (int64_t)n_frames * T, lrow, n_entries).total;
+  return layout((int64_t)n_frames * n_prims, (int64_t)n_frames * T, lrow, n_entries, n_frames).total;
 }
 
 int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cfg,
@@ -257,7 +258,19 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   if (FT >= (1LL << 31) || FN >= (1LL << 31))
     return set_error(SQV_ERR_ARG, "batch too large (split frames)");
   const int lrow = (cm + 1 + 3) & ~3;
-  Layout L = layout(FN, FT, lrow, 0);
+  Layout L = layout(FN, FT, lrow, 0, F);
+  // binning: for sparse batches (< 64 entries per tile on average, decided
+  // after the header readback) one CTA per frame (sqv_bin.cu) when the
+  // frame's tile counters fit shared memory (config 1 +3%); dense batches
+  // keep emit + radix sort, whose many short CTAs slot in under the previous
+  // batch's evaluation better than F long ones (per-frame binning measured
+  // config 2 -0.6%, config 3 -1.7%, config 4 -4.6%).  SQV_BIN=radix / frame
+  // force either (A/B, tests); SQV_BIN=fused also moves the block masks into
+  // the per-frame kernel (measured slower everywhere but config 1).
+  const char* benv = std::getenv("SQV_BIN");
+  const bool bin_radix = benv && std::strcmp(benv, "radix") == 0;
+  const bool bin_forced = benv && (std::strcmp(benv, "frame") == 0 || std::strcmp(benv, "fused") == 0);
+  const bool frame_ok = bin_frames_supported((int)T) && !bin_radix;
   if (ws_bytes < L.fixed_end || !workspace) {
     if (ws_needed) *ws_needed = L.total;
     return set_error(SQV_ERR_WORKSPACE, "workspace too small: need >= %zu bytes", L.total);
@@ -269,12 +282,14 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   int* windows = (int*)(ws + L.windows);
   int* tile_off = (int*)(ws + L.tile_off);
   int* scan_tmp = (int*)(ws + L.scan_tmp);
+  int* frame_count = (int*)(ws + L.frame_count);
   float* recs = (float*)(ws + L.recs);
   float* lrows = (float*)(ws + L.lrows);
 
   // header: zeros, bad_word = ~0 (memset kernels, no host copy)
   if (cudaMemsetAsync(hdr, 0, sizeof(Header), s) != cudaSuccess ||
-      cudaMemsetAsync(&hdr->bad_word, 0xFF, sizeof(hdr->bad_word), s) != cudaSuccess)
+      cudaMemsetAsync(&hdr->bad_word, 0xFF, sizeof(hdr->bad_word), s) != cudaSuccess ||
+      (frame_ok && cudaMemsetAsync(frame_count, 0, (size_t)F * 4, s) != cudaSuccess))
     return check_launch("workspace init");
   Header* hmap = mapped_header();
   if (!hmap) return set_error(SQV_ERR_CUDA, "mapped header allocation failed");
@@ -310,6 +325,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
     P.bad_word = &hdr->bad_word;
     P.n_pairs = &hdr->n_pairs;
     P.n_entries = reinterpret_cast<unsigned long long*>(&hdr->n_entries);
+    P.frame_count = frame_ok ? frame_count : nullptr;
     prep_kernel<<<div_up(FN, 128), 128, 0, s>>>(P);
     count_launch();
     if (int rc = check_launch("prep_kernel")) return rc;
@@ -338,7 +354,8 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   const int64_t E = h.n_entries;  // exact (64-bit atomics in prep)
   if (E < 0 || E >= (1LL << 31) - 1)
     return set_error(SQV_ERR_ARG, "too many bin entries: %lld (split frames)", (long long)E);
-  L = layout(FN, FT, lrow, E);
+  const bool frame_bin = frame_ok && (bin_forced || E < 64 * FT);
+  L = layout(FN, FT, lrow, E, F);
   if (ws_needed) *ws_needed = L.total;
   if (ws_bytes < L.total)
     return set_error(SQV_ERR_WORKSPACE, "workspace too small: need %zu bytes", L.total);
@@ -349,49 +366,79 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   int* radix_tmp = (int*)(ws + L.radix_tmp);
 
   if (prof) cudaEventRecord(g_prof.ev[pset][2], s);
-  // K3 emit + K4 radix sort + tile offsets
-  int which = 0;
-  if (E > 0) {
-    EmitArgs Em;
-    Em.n_frames = F;
-    Em.n_prims = N;
-    Em.tiles_per_frame = (int)T;
-    Em.ntx = ntx;
-    Em.nty = nty;
-    Em.counts = counts;
-    Em.offs = offs;
-    Em.windows = windows;
-    Em.keys = keys_a;
-    Em.vals = vals_a;
-    emit_kernel<<<(int)div_up(FN * 32, 256), 256, 0, s>>>(Em);
-    count_launch();
-    if (int rc = check_launch("emit_kernel")) return rc;
-    int bits = 0;
-    while (bits < 32 && (1LL << bits) < FT) ++bits;
-    if (int rc = radix_sort(keys_a, vals_a, keys_b, vals_b, E, bits, radix_tmp, &which, s))
-      return rc;
-  }
-  const int* sorted_vals = which ? vals_b : vals_a;
-  const uint32_t* sorted_keys = which ? keys_b : keys_a;
   // evaluator choice: tcgen05 by default; SQV_EVAL=ffma selects the
   // CUDA-core one (A/B runs).  The tensor cores accumulate with truncation:
   // the bias grows with the number of K steps per voxel (measured: about
   // -1e-8 relative per entry per tile, scripts/diag_depth.py).  Tiles deeper
   // than the precision mode allows go to the CUDA-core evaluator (FP32
   // round-to-nearest), launched after the tensor-core one on the same
-  // stream over the list tile_bounds_kernel builds.
+  // stream over the deep-tile list the binning builds.
   const char* ev = std::getenv("SQV_EVAL");
   const bool ffma = (ev && std::strcmp(ev, "ffma") == 0) || !eval_tc_supported(cm);
   int depth = cfg->precision ? 512 : 768;
   if (const char* de = std::getenv("SQV_TC_DEPTH")) depth = std::atoi(de);
   const bool complement = !ffma && E > depth && cm <= 32;
   int* deep = (int*)(ws + L.deep);
-  tile_bounds_kernel<<<div_up(FT + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off,
-                                                         complement ? depth : -1, deep,
-                                                         &hdr->deep_count);
-  count_launch();
-  if (int rc = check_launch("tile_bounds_kernel")) return rc;
   uint32_t* bmask = (uint32_t*)(ws + L.bmask);
+  const int* sorted_vals = vals_a;
+  const uint32_t* sorted_keys = keys_a;
+  if (frame_bin) {
+    // K3-K4b in one launch: per-frame counting sort, tile offsets, deep
+    // list and block masks (sqv_bin.cu)
+    BinArgs Bn;
+    Bn.n_frames = F;
+    Bn.n_prims = N;
+    Bn.tiles_per_frame = (int)T;
+    Bn.ntx = ntx;
+    Bn.nty = nty;
+    Bn.counts = counts;
+    Bn.windows = windows;
+    Bn.frame_count = frame_count;
+    Bn.keys = keys_a;
+    Bn.vals = vals_a;
+    Bn.tile_off = tile_off;
+    Bn.deep_min = complement ? depth : -1;
+    Bn.deep_tiles = deep;
+    Bn.deep_count = &hdr->deep_count;
+    Bn.recs = recs;
+    Bn.lrows = lrows;
+    Bn.lrow = lrow;
+    Bn.acc_c = cfg->precision ? SQV_ACC_C : INFINITY;
+    // (block masks in the binning kernel: SQV_BIN=fused; measured slower,
+    // the masks' per-entry field tests want the whole GPU, not F CTAs)
+    Bn.bmask = (!ffma && benv && std::strcmp(benv, "fused") == 0) ? bmask : nullptr;
+    if (int rc = bin_frames_launch(Bn, s)) return rc;
+  } else {
+    // K3 emit + K4 radix sort + tile offsets
+    int which = 0;
+    if (E > 0) {
+      EmitArgs Em;
+      Em.n_frames = F;
+      Em.n_prims = N;
+      Em.tiles_per_frame = (int)T;
+      Em.ntx = ntx;
+      Em.nty = nty;
+      Em.counts = counts;
+      Em.offs = offs;
+      Em.windows = windows;
+      Em.keys = keys_a;
+      Em.vals = vals_a;
+      emit_kernel<<<(int)div_up(FN * 32, 256), 256, 0, s>>>(Em);
+      count_launch();
+      if (int rc = check_launch("emit_kernel")) return rc;
+      int bits = 0;
+      while (bits < 32 && (1LL << bits) < FT) ++bits;
+      if (int rc = radix_sort(keys_a, vals_a, keys_b, vals_b, E, bits, radix_tmp, &which, s))
+        return rc;
+    }
+    sorted_vals = which ? vals_b : vals_a;
+    sorted_keys = which ? keys_b : keys_a;
+    tile_bounds_kernel<<<div_up(FT + 1, 256), 256, 0, s>>>(sorted_keys, E, FT, tile_off,
+                                                           complement ? depth : -1, deep,
+                                                           &hdr->deep_count);
+    count_launch();
+    if (int rc = check_launch("tile_bounds_kernel")) return rc;
+  }
 
   // K5 evaluate + finalize
   EvalArgs A;
@@ -426,7 +473,7 @@ int sqv_voxelize(const sqv_prims* prims, const sqv_grid* grid, const sqv_cfg* cf
   if (prof) cudaEventRecord(g_prof.ev[pset][3], s);
   {
     A.bmask = bmask;
-    if (!ffma && E > 0)
+    if (!ffma && E > 0 && !(frame_bin && benv && std::strcmp(benv, "fused") == 0))
       if (int rc = block_masks_launch(sorted_keys, sorted_vals, E, recs, lrows, lrow, tile_off,
                                       (int)T, ntx, nty, N,
                                       cfg->precision ? SQV_ACC_C : INFINITY, bmask, s))

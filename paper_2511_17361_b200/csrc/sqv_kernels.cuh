@@ -22,7 +22,31 @@ struct PrepArgs {
   // 64-bit sum of counts[]: the (tile, primitive) entry total, checked on the
   // host before the 32-bit scan offsets and emit are trusted
   unsigned long long* n_entries;
+  int* frame_count;  // [F] entries per frame (per-frame binning), or NULL
 };
+
+// per-frame binning (sqv_bin.cu): tile lists, offsets, deep list, masks
+struct BinArgs {
+  int n_frames, n_prims;
+  int tiles_per_frame, ntx, nty;
+  const int* counts;       // [FN] tiles per primitive (prep)
+  const int* windows;      // [FN][6] clipped voxel windows (prep)
+  const int* frame_count;  // [F] entries per frame (prep)
+  uint32_t* keys;          // [E] global tile id per entry
+  int* vals;               // [E] frame-local primitive id per entry
+  int* tile_off;           // [F*T + 1]
+  int deep_min;            // tiles with more entries go to deep_tiles (-1: none)
+  int* deep_tiles;
+  int* deep_count;
+  const float* recs;       // block masks (bmask NULL: none)
+  const float* lrows;
+  int lrow;
+  float acc_c;
+  uint32_t* bmask;
+};
+size_t bin_frames_smem(int tiles_per_frame);
+bool bin_frames_supported(int tiles_per_frame);
+int bin_frames_launch(const BinArgs& A, cudaStream_t s);
 
 struct EmitArgs {
   int n_frames, n_prims;

@@ -50,6 +50,92 @@ __device__ __forceinline__ bool block_inside(const PrimRec& R, int bx0, int by0,
          (bz0 >= R.lo[2]) & (bz0 + 7 <= R.hi[2]);
 }
 
+// The block mask of one (tile, primitive) entry: which of the 8x8x16 tile's
+// 8 warp blocks (4x4x8, bit b = (z half, y half, x half)) the primitive can
+// reach (bits 0-7), which lie wholly inside its window (bits 8-15), and
+// strict mode's accurate-log flag (bit 16, c > acc_c).  The cull decisions
+// are block_may_hit's (window overlap, the Chebyshev box bound, the
+// nearest-corner field bound, all conservative), with the shared parts
+// computed once per entry (the 8 local block centres differ by fixed lattice
+// steps); a block whose nearest local corner is deep inside — (2^b + 1)
+// max|x'|^c well below the cut — is marked without the 8-MUFU field test.
+// A "hit" that could have been culled only costs evaluation work: those
+// pairs get their exact FP32 w.  rec: the primitive's record (global),
+// wmax: its class-weight padding column, e_tile: the tile's entry count.
+__device__ __forceinline__ uint32_t entry_block_mask(const float* rec, float wmax, int e_tile,
+                                                     int tx, int ty, int tz, float acc_c) {
+  PrimRec R;
+  const float4* src = reinterpret_cast<const float4*>(rec);
+  float4* dst = reinterpret_cast<float4*>(&R);
+#pragma unroll
+  for (int q = 0; q < kRecWords / 4; ++q) dst[q] = __ldg(src + q);
+  const int x0 = tx * kTileX, y0 = ty * kTileY, z0 = tz * kTileZ;
+  float ex[3], ey[3], ez[3], c0[3], h[3], stepx[3], stepy[3], stepz[3];
+  const float kx = (float)x0 + 1.5f - R.cx, ky = (float)y0 + 1.5f - R.cy,
+              kz = (float)z0 + 3.5f - R.cz;
+  float span = 0.0f;  // bounds |c| + h of every block: one FP32 error margin per entry
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    ex[r] = R.HL[3 * r].x + R.HL[3 * r].y;
+    ey[r] = R.HL[3 * r + 1].x + R.HL[3 * r + 1].y;
+    ez[r] = R.HL[3 * r + 2].x + R.HL[3 * r + 2].y;
+    c0[r] = fmaf(kz, ez[r], fmaf(ky, ey[r], fmaf(kx, ex[r], R.G[r].x + R.G[r].y)));
+    h[r] = 1.5f * fabsf(ex[r]) + 1.5f * fabsf(ey[r]) + 3.5f * fabsf(ez[r]);
+    stepx[r] = 4.0f * ex[r];
+    stepy[r] = 4.0f * ey[r];
+    stepz[r] = 8.0f * ez[r];
+    span += fabsf(c0[r]) + fabsf(stepx[r]) + fabsf(stepy[r]) + fabsf(stepz[r]) + h[r];
+  }
+  const float eps = 1e-4f * span;  // FP32 error of c, h (incl. the stepped centres)
+  const float cut = R.mcut + eps;
+  // The field threshold of this (tile, primitive) entry.  At most E_tile
+  // primitives reach a voxel of this tile, so cut = ln(E_tile wmax / 2e-12)
+  // keeps the dropped mass per voxel < 2e-12 (wmax rides in the class-weight
+  // row's padding column, written by prep; +0.01 covers __logf's error).
+  // The primitive's own (N-based) threshold mcut^c is the upper limit.
+  const float cut_f = fminf(ex2(R.c * lg2(R.mcut)),
+                            __logf((float)e_tile * wmax) + (float)kLnInvDropBound + 0.01f);
+  // window overlap / containment of the two block positions on each axis
+  const int* lo = R.lo;
+  const int* hi = R.hi;
+  const bool wx[2] = {x0 + 3 >= lo[0] && x0 <= hi[0], x0 + 7 >= lo[0] && x0 + 4 <= hi[0]};
+  const bool wy[2] = {y0 + 3 >= lo[1] && y0 <= hi[1], y0 + 7 >= lo[1] && y0 + 4 <= hi[1]};
+  const bool wz[2] = {z0 + 7 >= lo[2] && z0 <= hi[2], z0 + 15 >= lo[2] && z0 + 8 <= hi[2]};
+  const bool ix[2] = {x0 >= lo[0] && x0 + 3 <= hi[0], x0 + 4 >= lo[0] && x0 + 7 <= hi[0]};
+  const bool iy[2] = {y0 >= lo[1] && y0 + 3 <= hi[1], y0 + 4 >= lo[1] && y0 + 7 <= hi[1]};
+  const bool iz[2] = {z0 >= lo[2] && z0 + 7 <= hi[2], z0 + 8 >= lo[2] && z0 + 15 <= hi[2]};
+  // sure-hit radius: (2^b + 1) M^c <= 0.5 kFCut  <=>  M <= (0.5 kFCut / (2^b + 1))^(1/c)
+  const float inv_c = 1.0f / R.c;
+  const float sure = ex2(inv_c * lg2(0.5f * cut_f / (ex2(R.b) + 1.0f)));
+  unsigned m = 0;
+#pragma unroll
+  for (int bb = 0; bb < 8; ++bb) {
+    const int ox = bb & 1, oy = (bb >> 1) & 1, oz = bb >> 2;
+    if (!(wx[ox] && wy[oy] && wz[oz])) continue;
+    float mm[3], dmax = -1.0f;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      float c = c0[r];
+      if (ox) c += stepx[r];
+      if (oy) c += stepy[r];
+      if (oz) c += stepz[r];
+      mm[r] = fabsf(c) - h[r];
+      dmax = fmaxf(dmax, mm[r]);
+    }
+    if (dmax > cut) continue;
+    bool hit = dmax <= sure;
+    if (!hit) {
+      const float F = field_F(fmaxf(mm[0] - eps, 0.0f), fmaxf(mm[1] - eps, 0.0f),
+                              fmaxf(mm[2] - eps, 0.0f), R.a, R.b, R.c);
+      hit = F < 1.02f * cut_f;
+    }
+    if (hit) m |= (1u << bb) | ((unsigned)(ix[ox] && iy[oy] && iz[oz]) << (8 + bb));
+  }
+  // strict mode: the evaluator's accurate-log list (FMA-pipe logs for c > acc_c)
+  if (m && R.c > acc_c) m |= 1u << 16;
+  return m;
+}
+
 // ---- packed FP32x2 helpers (FFMA2 / FADD2 / FMUL2: two lanes of work per
 // issue slot; same IEEE round-to-nearest results as the scalar ops) --------
 __device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }

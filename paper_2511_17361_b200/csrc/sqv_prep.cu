@@ -186,6 +186,15 @@ __global__ void prep_kernel(PrepArgs A) {
     if (v) atomicAdd(A.n_pairs, v);
     if (e) atomicAdd(A.n_entries, e);
   }
+  // entries per frame (the per-frame binning's frame bases): one atomic per
+  // frame segment of the warp (a warp spans at most a few frames)
+  if (A.frame_count) {
+    const int f = gi < FN ? (int)(gi / A.n_prims) : -1;
+    const int c = gi < FN ? A.counts[gi] : 0;
+    const unsigned peers = __match_any_sync(0xffffffffu, f);
+    const int sum = __reduce_add_sync(peers, c);
+    if (f >= 0 && sum && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&A.frame_count[f], sum);
+  }
 }
 
 // K3: one thread per primitive; entries in (tz, ty, tx) order, primitive

@@ -474,11 +474,13 @@ def test_randomized_configurations(case):
     # or streaming
     os.environ["SQV_PERSIST"] = str(case % 2)
     os.environ["SQV_STREAM"] = str((case // 2) % 2)
+    os.environ["SQV_BIN"] = ("radix", "frame")[(case // 4) % 2]  # both binning paths
     try:
         out = _run(b, spec, cfg, C, truncate=truncate, bins=True)
     finally:
         del os.environ["SQV_PERSIST"]
         del os.environ["SQV_STREAM"]
+        del os.environ["SQV_BIN"]
     ref, grid = _oracle(b, spec, cfg, out["free_code"], truncate=truncate)
     np.testing.assert_array_equal(out["windows"], ref["windows"])
     off, ids = O.bins(ref["windows"], grid.dims)
@@ -530,11 +532,13 @@ def test_randomized_dense_configurations(case):
                emin=float(rng.choice([0.1, 0.2])))
     os.environ["SQV_PERSIST"] = str(case % 2)  # deep tiles in every evaluator variant
     os.environ["SQV_STREAM"] = str((case // 2) % 2)
+    os.environ["SQV_BIN"] = ("radix", "frame", "fused")[(case // 4) % 3]
     try:
         out = _run(b, spec, cfg, C, bins=True)
     finally:
         del os.environ["SQV_PERSIST"]
         del os.environ["SQV_STREAM"]
+        del os.environ["SQV_BIN"]
     ref, grid = _oracle(b, spec, cfg, out["free_code"])
     off, ids = O.bins(ref["windows"], grid.dims)
     np.testing.assert_array_equal(out["tile_off"], off)
@@ -665,3 +669,23 @@ def test_evaluator_work_counters():
     vox(b, dense=False)  # detached: counters unchanged
     torch.cuda.synchronize()
     assert int(st[0]) == mufu
+
+
+@pytest.mark.parametrize("n_prims", [256, 2000])
+def test_binning_paths_bit_identical(monkeypatch, n_prims):
+    """Per-frame counting-sort binning (sqv_bin.cu, with and without the
+    fused block masks) and emit + radix sort give the same bins, masks and
+    outputs bit for bit."""
+    P = _pkg()
+    from paper_2511_17361_b200.scenegen import gen_frames
+    spec = P.VoxelGridSpec()
+    b = gen_frames(71, 3, n_prims)
+    outs = []
+    for mode in ("radix", "frame", "fused"):
+        monkeypatch.setenv("SQV_BIN", mode)
+        r = P.Voxelizer(spec, P.VoxelizeConfig(), 18)(b, dense=True, bins=True)
+        outs.append([r.labels.cpu().numpy(), r.v_c.cpu().numpy(),
+                     *(r.bins[k].cpu().numpy() for k in ("windows", "tile_off", "prim_ids"))])
+    for o in outs[1:]:
+        for x, y in zip(outs[0], o):
+            np.testing.assert_array_equal(x, y)
