@@ -150,10 +150,16 @@ struct Profiler {
   int next = 0;
   double ms[SQV_NSTAGES] = {0, 0, 0, 0, 0};
   long long calls = 0;
+  // SQV_PROF_TRACE (diagnostics): print every folded call's stage events as
+  // times (ms) since sqv_profile_enable — prep, after the count scan, after
+  // the readback, before the masks, after the evaluator, after the masks
+  cudaEvent_t ref;
+  bool trace = false;
   void ensure() {
     if (!created) {
       for (auto& set : ev)
         for (auto& e : set) cudaEventCreate(&e);
+      cudaEventCreate(&ref);
       created = true;
     }
   }
@@ -163,6 +169,11 @@ struct Profiler {
     return m;
   }
   void fold(int i) {
+    if (trace) {
+      fprintf(stderr, "sqv trace call %lld:", calls);
+      for (int k = 0; k < 6; ++k) fprintf(stderr, " %.3f", el(ref, ev[i][k]));
+      fprintf(stderr, "\n");
+    }
     const double m0 = el(ev[i][0], ev[i][1]), m1 = el(ev[i][2], ev[i][3]),
                  m2 = el(ev[i][3], ev[i][4]), m4 = el(ev[i][5], ev[i][4]);
     ms[0] += m0;
@@ -623,6 +634,11 @@ int sqv_stats_attach(int64_t* counters) {
 int sqv_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   g_prof.on = on != 0;
+  if (g_prof.on) {
+    g_prof.ensure();
+    g_prof.trace = std::getenv("SQV_PROF_TRACE") != nullptr;
+    cudaEventRecord(g_prof.ref, 0);
+  }
   return SQV_OK;
 }
 
