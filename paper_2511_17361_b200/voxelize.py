@@ -225,15 +225,27 @@ class Voxelizer:
         cur.wait_stream(self._side)
 
     # ---- pipelined host streams ----------------------------------------------
-    def stream(self, batches, *, dense: bool = True, on_device=None, labels_out=None):
+    def stream(self, batches, *, dense: bool = True, on_device=None, labels_out=None,
+               edge_pieces: int = 4):
         """Voxelize a sequence of host batches (pinned torch tensors for real
         overlap) with copies overlapped: the H2D copy of batch k+1 and the D2H
         copy of batch k-1's labels run on two copy streams while batch k is
         evaluated; consecutive batches alternate two compute streams (the
         current one and a side stream, as in ``run_many``) so a batch's
-        binning overlaps the previous evaluation.  ``on_device(k, result)`` is
-        called on batch k's compute stream right after it (e.g. confusion
-        counts).
+        binning overlaps the previous evaluation.  Input slots and device
+        label buffers are triple-buffered: batch k's binning waits only for
+        copies that finished a whole batch earlier, so it is ready to run the
+        moment batch k-2's evaluation ends (with double buffers it also waited
+        for batch k-2's label D2H / batch k's H2D, issued only then, and lost
+        its slot to batch k-1's evaluation).  The first and the last batch run
+        as ``edge_pieces`` frame ranges (alternating the two compute streams
+        too), so evaluation starts after the first range's H2D copy and only
+        the last range's labels are copied after the final evaluation: the
+        pipeline fills and drains at a quarter of a batch.  (Per-frame
+        results depend on the frame grouping only through the evaluator's
+        density-based kernel choice, see sqv_eval_tc_impl.cuh launch_tc.)
+        ``on_device(k, result)`` is called once per batch, on its compute
+        stream, after all of it (e.g. confusion counts).
         Returns the host label tensors [F, nz, ny, nx] (uint8, pinned), valid
         when this call returns."""
         t = self.torch
@@ -251,49 +263,94 @@ class Voxelizer:
                      else t.from_numpy(np.ascontiguousarray(getattr(b, k))))
                  for k in PrimitiveBatch.FIELDS} for b in batches]
         shapes = {k: (tuple(v.shape), v.dtype) for k, v in host[0].items()}
+        F = batches[0].n_frames
+        NS = min(3, nb)  # input slots / device label buffers
         slots = [{k: t.empty(s, dtype=t.float64, device=self.device) for k, (s, _) in
-                  shapes.items()} for _ in range(2)]
-        outs = [self.alloc(batches[0].n_frames, dense) for _ in range(2)]
+                  shapes.items()} for _ in range(NS)]
+        dense_out = [self.alloc(F, dense) for _ in range(min(2, nb))]  # per compute stream
+        labs = [o.labels for o in dense_out] + [
+            t.empty((F, nz, ny, nx), dtype=t.uint8, device=self.device)
+            for _ in range(NS - len(dense_out))]
         if labels_out is None:
             labels_out = [t.empty((b.n_frames, nz, ny, nx), dtype=t.uint8).pin_memory()
                           for b in batches]
-        ev_h2d = [None, None]
-        ev_in_free = [None, None]
-        ev_out_free = [None, None]
+        n_edge = max(1, min(int(edge_pieces), F // 8))  # pieces of >= 8 frames
+
+        def ranges(k):
+            n = n_edge if k in (0, nb - 1) else 1
+            cut = [F * j // n for j in range(n + 1)]
+            return list(zip(cut[:-1], cut[1:]))
+
+        ev_h2d = [[] for _ in range(NS)]       # per input slot: one event per range
+        ev_in_free = [None] * NS               # batch done: its input slot may be refilled
+        ev_out_free = [None] * NS              # label D2H done: the buffer may be rewritten
+        ev_done = {}
 
         def load(k):
-            s = k & 1
+            q = k % NS
             if tuple(host[k]["opacity"].shape) != shapes["opacity"][0]:
                 raise ValueError("all batches of a stream must have the same shape")
             with t.cuda.stream(h2d):
-                if ev_in_free[s] is not None:
-                    h2d.wait_event(ev_in_free[s])
-                for f, v in host[k].items():
-                    slots[s][f].copy_(v, non_blocking=True)
-                ev_h2d[s] = h2d.record_event()
+                if ev_in_free[q] is not None:
+                    h2d.wait_event(ev_in_free[q])
+                ev_h2d[q] = []
+                for lo, hi in ranges(k):
+                    for f, v in host[k].items():
+                        slots[q][f][lo:hi].copy_(v[lo:hi], non_blocking=True)
+                    ev_h2d[q].append(h2d.record_event())
 
+        part = lambda a, lo, hi: None if a is None else a[lo:hi]
         load(0)
         for k in range(nb):
-            s = k & 1
+            s, q = k & 1, k % NS
             if k + 1 < nb:
                 load(k + 1)
+            # n_valid stays on the host: each call copies its range on its own stream
+            full = PrimitiveBatch(*(slots[q][f] for f in PrimitiveBatch.FIELDS),
+                                  n_valid=batches[k].n_valid)
+            out = VoxelizeResult(labs[q], dense_out[s].v_o, dense_out[s].v_c, self.free_code)
+            rs = ranges(k)
+            used, last_d2h = set(), None
+            n_pairs = n_entries = 0
+            for j, (lo, hi) in enumerate(rs):
+                # a single range keeps the batch's stream; edge ranges alternate
+                ci = s if len(rs) == 1 else (s + j) & 1
+                comp = comps[ci]
+                with t.cuda.stream(comp):
+                    comp.wait_event(ev_h2d[q][j])
+                    if ev_out_free[q] is not None:
+                        comp.wait_event(ev_out_free[q])
+                    if ci != s and ci not in used and k >= 2:
+                        comp.wait_event(ev_done[k - 2])  # the dense slot's last user
+                    used.add(ci)
+                    sub = full if len(rs) == 1 else full.frames(lo, hi)
+                    view = out if len(rs) == 1 else VoxelizeResult(
+                        out.labels[lo:hi], part(out.v_o, lo, hi), part(out.v_c, lo, hi))
+                    r = self(sub, dense=dense, out=view, _slot=ci)
+                    n_pairs += r.n_pairs
+                    n_entries += r.n_entries
+                    piece_done = comp.record_event()
+                if k == nb - 1 and len(rs) > 1:  # the last batch's labels per range
+                    with t.cuda.stream(d2h):
+                        d2h.wait_event(piece_done)
+                        labels_out[k][lo:hi].copy_(out.labels[lo:hi], non_blocking=True)
+                        last_d2h = d2h.record_event()
             comp = comps[s]
             with t.cuda.stream(comp):
-                comp.wait_event(ev_h2d[s])
-                if ev_out_free[s] is not None:
-                    comp.wait_event(ev_out_free[s])
-                nv = batches[k].n_valid
-                db = PrimitiveBatch(*(slots[s][f] for f in PrimitiveBatch.FIELDS),
-                                    n_valid=None if nv is None else self._dev(nv, t.int32))
-                res = self(db, dense=dense, out=outs[s], _slot=s)
+                for ci in used - {s}:
+                    comp.wait_stream(comps[ci])
+                out.n_pairs, out.n_entries = n_pairs, n_entries
                 if on_device is not None:
-                    on_device(k, res)
+                    on_device(k, out)
                 done = comp.record_event()
-            ev_in_free[s] = done
-            with t.cuda.stream(d2h):
-                d2h.wait_event(done)
-                labels_out[k].copy_(outs[s].labels, non_blocking=True)
-                ev_out_free[s] = d2h.record_event()
+            ev_done[k] = ev_in_free[q] = done
+            ev_done.pop(k - 3, None)
+            if last_d2h is None:
+                with t.cuda.stream(d2h):
+                    d2h.wait_event(done)
+                    labels_out[k].copy_(out.labels, non_blocking=True)
+                    last_d2h = d2h.record_event()
+            ev_out_free[q] = last_d2h
         d2h.synchronize()
         comps[1].synchronize()
         comp0.wait_stream(comps[1])

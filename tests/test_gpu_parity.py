@@ -358,6 +358,46 @@ def test_stream_api_matches_direct_calls():
         assert torch.equal(direct, lab)
 
 
+@pytest.mark.parametrize("nb,ragged", [(1, False), (2, False), (4, False), (4, True)])
+def test_stream_edge_ranges_match_direct_calls(nb, ragged, monkeypatch):
+    """Voxelizer.stream splits its first and last batch into frame ranges
+    (pipeline fill/drain) and triple-buffers inputs and labels: labels, v_o,
+    v_c and the pair counts handed to on_device equal one direct call per
+    batch, bit for bit.  The evaluator kernel is pinned (SQV_STREAM=1): its
+    automatic choice depends on the batch's density and tile count, and the
+    chunk-staged and streaming kernels agree to rounding, not bit for bit."""
+    import torch
+    monkeypatch.setenv("SQV_STREAM", "1")
+    P = _pkg()
+    spec = P.VoxelGridSpec((-8.0, -8.0, -2.0), (40, 40, 16), 0.4)
+    vox = P.Voxelizer(spec, P.VoxelizeConfig(), 6)
+    F = 40
+    batches = []
+    for k in range(nb):
+        b = _scene(90 + k, 150, C=6, frames=F, origin=spec.origin, dims=spec.dims, smax=2.0)
+        if ragged:
+            b = P.PrimitiveBatch(b.mu, b.scale, b.rot, b.opacity, b.eps, b.logits,
+                                 n_valid=np.random.default_rng(k).integers(0, 151, F)
+                                 .astype(np.int32))
+        batches.append(b)
+    pinned = [P.PrimitiveBatch(**{f: torch.from_numpy(np.asarray(getattr(b, f))).pin_memory()
+                                  for f in P.PrimitiveBatch.FIELDS}, n_valid=b.n_valid)
+              for b in batches]
+    got = {}
+
+    def cb(k, r):
+        got[k] = (r.v_o.clone(), r.v_c.clone(), r.n_pairs, r.n_entries)
+
+    labels = vox.stream(pinned, on_device=cb, edge_pieces=4)
+    torch.cuda.synchronize()
+    assert sorted(got) == list(range(nb))
+    for k, (b, lab) in enumerate(zip(batches, labels)):
+        d = vox(b)
+        assert torch.equal(d.labels.cpu(), lab)
+        assert torch.equal(d.v_o, got[k][0]) and torch.equal(d.v_c, got[k][1])
+        assert (d.n_pairs, d.n_entries) == got[k][2:]
+
+
 def test_truncation_report_soundness():
     """cmd_voxelize --oracle: omitted mass is non-negative,
     every label flip lost mass, and the omitted mass stays under the summed
