@@ -264,13 +264,16 @@ class Voxelizer:
                  for k in PrimitiveBatch.FIELDS} for b in batches]
         shapes = {k: (tuple(v.shape), v.dtype) for k, v in host[0].items()}
         F = batches[0].n_frames
-        NS = min(3, nb)  # input slots / device label buffers
+        # input slots / device label buffers; the same allocations for any
+        # number of batches, so the caching allocator reuses the previous
+        # call's blocks (a different pattern makes it map new memory inside
+        # the caller's timed loop)
+        NS = 3
         slots = [{k: t.empty(s, dtype=t.float64, device=self.device) for k, (s, _) in
                   shapes.items()} for _ in range(NS)]
-        dense_out = [self.alloc(F, dense) for _ in range(min(2, nb))]  # per compute stream
+        dense_out = [self.alloc(F, dense) for _ in range(2)]  # per compute stream
         labs = [o.labels for o in dense_out] + [
-            t.empty((F, nz, ny, nx), dtype=t.uint8, device=self.device)
-            for _ in range(NS - len(dense_out))]
+            t.empty((F, nz, ny, nx), dtype=t.uint8, device=self.device)]
         if labels_out is None:
             labels_out = [t.empty((b.n_frames, nz, ny, nx), dtype=t.uint8).pin_memory()
                           for b in batches]
