@@ -729,6 +729,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
     int end = A.tile_off[tile_g + 1];
     if (end - beg > A.tc_max_entries) end = beg;
     const int fbase = f * A.n_prims;
+#ifdef SQV_DIAG_IMBAL
+    int diag_items = 0;
+#endif
     for (int c0 = beg; c0 < end; c0 += S::kSeg) {
       const int n = min(S::kSeg, end - c0);
       // ---- this warp's sequence of the segment, from the block masks:
@@ -778,6 +781,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
       // right before its first item is read, and batch b+1 is issued once
       // batch b-1 has been read (its half of the ring is free) ----
       const int n_seq = n_in + n_part + n_acc;
+#ifdef SQV_DIAG_IMBAL
+      diag_items += n_seq;
+#endif
       if (lane == 0)
         add_stats(A.stats, (n_in + n_part) * mufu_per_block(FIELD, false) +
                                n_acc * mufu_per_block(FIELD, true), n_seq);
@@ -905,9 +911,21 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) eval_tcs_kernel(EvalArgs A) 
     wait_free();
     if (lane == 0) s_has[warp] = groups > 0;
     if (PERSIST && tid == 0) *s_next = (int)gridDim.x + claimed;
+#ifdef SQV_DIAG_IMBAL  // diagnostics: stats[2] += max over warps, stats[3] += sum
+    __shared__ int s_diag[NW];
+    if (lane == 0) s_diag[warp] = diag_items;
+#endif
     tc::fence_before_sync();
     __syncthreads();  // all MMAs complete; operand smem is free for staging
     tc::fence_after_sync();
+#ifdef SQV_DIAG_IMBAL
+    if (tid == 0 && A.stats) {
+      int mx = 0, sm = 0;
+      for (int w = 0; w < NW; ++w) mx = max(mx, s_diag[w]), sm += s_diag[w];
+      atomicAdd(A.stats + 2, (unsigned long long)mx);
+      atomicAdd(A.stats + 3, (unsigned long long)sm);
+    }
+#endif
     const int next_item = PERSIST ? *s_next : n_items;
     tile_epilogue<CM, NW>(A, smem, s_has, tmem_base, warp, lane, f, tx, ty, tz, half * 8);
     if (PERSIST && next_item < n_items) {
