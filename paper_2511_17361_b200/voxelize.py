@@ -303,61 +303,65 @@ class Voxelizer:
                     ev_h2d[q].append(h2d.record_event())
 
         part = lambda a, lo, hi: None if a is None else a[lo:hi]
-        load(0)
-        for k in range(nb):
-            s, q = k & 1, k % NS
-            if k + 1 < nb:
-                load(k + 1)
-            # n_valid stays on the host: each call copies its range on its own stream
-            full = PrimitiveBatch(*(slots[q][f] for f in PrimitiveBatch.FIELDS),
-                                  n_valid=batches[k].n_valid)
-            out = VoxelizeResult(labs[q], dense_out[s].v_o, dense_out[s].v_c, self.free_code)
-            rs = ranges(k)
-            used, last_d2h = set(), None
-            n_pairs = n_entries = 0
-            for j, (lo, hi) in enumerate(rs):
-                # a single range keeps the batch's stream; edge ranges alternate
-                ci = s if len(rs) == 1 else (s + j) & 1
-                comp = comps[ci]
+        try:
+            load(0)
+            for k in range(nb):
+                s, q = k & 1, k % NS
+                if k + 1 < nb:
+                    load(k + 1)
+                # n_valid stays on the host: each call copies its range on its own stream
+                full = PrimitiveBatch(*(slots[q][f] for f in PrimitiveBatch.FIELDS),
+                                      n_valid=batches[k].n_valid)
+                out = VoxelizeResult(labs[q], dense_out[s].v_o, dense_out[s].v_c, self.free_code)
+                rs = ranges(k)
+                used, last_d2h = set(), None
+                n_pairs = n_entries = 0
+                for j, (lo, hi) in enumerate(rs):
+                    # a single range keeps the batch's stream; edge ranges alternate
+                    ci = s if len(rs) == 1 else (s + j) & 1
+                    comp = comps[ci]
+                    with t.cuda.stream(comp):
+                        comp.wait_event(ev_h2d[q][j])
+                        if ev_out_free[q] is not None:
+                            comp.wait_event(ev_out_free[q])
+                        if ci != s and ci not in used and k >= 2:
+                            comp.wait_event(ev_done[k - 2])  # the dense slot's last user
+                        used.add(ci)
+                        sub = full if len(rs) == 1 else full.frames(lo, hi)
+                        view = out if len(rs) == 1 else VoxelizeResult(
+                            out.labels[lo:hi], part(out.v_o, lo, hi), part(out.v_c, lo, hi))
+                        r = self(sub, dense=dense, out=view, _slot=ci, _frame0=lo)
+                        n_pairs += r.n_pairs
+                        n_entries += r.n_entries
+                        piece_done = comp.record_event()
+                    if k == nb - 1 and len(rs) > 1:  # the last batch's labels per range
+                        with t.cuda.stream(d2h):
+                            d2h.wait_event(piece_done)
+                            labels_out[k][lo:hi].copy_(out.labels[lo:hi], non_blocking=True)
+                            last_d2h = d2h.record_event()
+                comp = comps[s]
                 with t.cuda.stream(comp):
-                    comp.wait_event(ev_h2d[q][j])
-                    if ev_out_free[q] is not None:
-                        comp.wait_event(ev_out_free[q])
-                    if ci != s and ci not in used and k >= 2:
-                        comp.wait_event(ev_done[k - 2])  # the dense slot's last user
-                    used.add(ci)
-                    sub = full if len(rs) == 1 else full.frames(lo, hi)
-                    view = out if len(rs) == 1 else VoxelizeResult(
-                        out.labels[lo:hi], part(out.v_o, lo, hi), part(out.v_c, lo, hi))
-                    r = self(sub, dense=dense, out=view, _slot=ci)
-                    n_pairs += r.n_pairs
-                    n_entries += r.n_entries
-                    piece_done = comp.record_event()
-                if k == nb - 1 and len(rs) > 1:  # the last batch's labels per range
+                    for ci in used - {s}:
+                        comp.wait_stream(comps[ci])
+                    out.n_pairs, out.n_entries = n_pairs, n_entries
+                    if on_device is not None:
+                        on_device(k, out)
+                    done = comp.record_event()
+                ev_done[k] = ev_in_free[q] = done
+                ev_done.pop(k - 3, None)
+                if last_d2h is None:
                     with t.cuda.stream(d2h):
-                        d2h.wait_event(piece_done)
-                        labels_out[k][lo:hi].copy_(out.labels[lo:hi], non_blocking=True)
+                        d2h.wait_event(done)
+                        labels_out[k].copy_(out.labels, non_blocking=True)
                         last_d2h = d2h.record_event()
-            comp = comps[s]
-            with t.cuda.stream(comp):
-                for ci in used - {s}:
-                    comp.wait_stream(comps[ci])
-                out.n_pairs, out.n_entries = n_pairs, n_entries
-                if on_device is not None:
-                    on_device(k, out)
-                done = comp.record_event()
-            ev_done[k] = ev_in_free[q] = done
-            ev_done.pop(k - 3, None)
-            if last_d2h is None:
-                with t.cuda.stream(d2h):
-                    d2h.wait_event(done)
-                    labels_out[k].copy_(out.labels, non_blocking=True)
-                    last_d2h = d2h.record_event()
-            ev_out_free[q] = last_d2h
-        d2h.synchronize()
-        comps[1].synchronize()
+                ev_out_free[q] = last_d2h
+        finally:
+            # also on an error: no buffer of this call is released (and
+            # reused by the caching allocator) while a copy or compute stream
+            # may still use it
+            for st in (h2d, d2h, comps[1], comp0):
+                st.synchronize()
         comp0.wait_stream(comps[1])
-        comp0.synchronize()
         return labels_out
 
     # ---- run ----------------------------------------------------------------
@@ -372,7 +376,8 @@ class Voxelizer:
         return out
 
     def __call__(self, batch: PrimitiveBatch, *, dense: bool = True, bins: bool = False,
-                 out: VoxelizeResult | None = None, _slot: int = 0) -> VoxelizeResult:
+                 out: VoxelizeResult | None = None, _slot: int = 0,
+                 _frame0: int = 0) -> VoxelizeResult:
         """Voxelize F frames.  Host inputs are copied to the device first
         (non_blocking from pinned memory).  ``out`` may be preallocated with
         ``alloc``; ``dense=False`` keeps v_o/v_c on chip (labels only)."""
@@ -381,7 +386,7 @@ class Voxelizer:
             raise ValueError(f"batch has {batch.n_classes} classes, voxelizer expects {self.C}")
         with t.cuda.device(self.device):
             try:
-                return self._run(batch, dense, bins, out, _slot)
+                return self._run(batch, dense, bins, out, _slot, _frame0)
             except _lib.SqvError as e:
                 # index spaces are 32-bit per call: halve the frames and retry
                 if "split frames" not in str(e) or batch.n_frames < 2 or bins:
@@ -392,14 +397,17 @@ class Voxelizer:
             part = lambda a, lo, hi: None if a is None else a[lo:hi]
             rs = [self(batch.frames(lo, hi), dense=dense,
                        out=VoxelizeResult(out.labels[lo:hi], part(out.v_o, lo, hi),
-                                          part(out.v_c, lo, hi)), _slot=_slot)
+                                          part(out.v_c, lo, hi)), _slot=_slot,
+                       _frame0=_frame0 + lo)
                   for lo, hi in ((0, h), (h, F))]
             out.free_code = self.free_code
             out.n_pairs = sum(r.n_pairs for r in rs)
             out.n_entries = sum(r.n_entries for r in rs)
             return out
 
-    def _run(self, batch, dense, bins, out, slot=0):
+    def _run(self, batch, dense, bins, out, slot=0, frame0=0):
+        """One sqv_voxelize call; frame0 = the batch's first frame in the
+        caller's batch (a range of it), for error messages."""
         t = self.torch
         db = self.to_device(batch)
         F, N = db.n_frames, db.n_prims
@@ -447,6 +455,7 @@ class Voxelizer:
                 continue
             if rc == _lib.SQV_ERR_INVALID_PRIM:
                 f, i = divmod(int(bad_prim.value), max(N, 1))
+                f += frame0
                 raise ValueError(f"frame {f} primitive {i}: "
                                  f"{bad_bits_message(int(bad_bits.value))}")
             _lib.check(rc, "sqv_voxelize")

@@ -398,6 +398,33 @@ def test_stream_edge_ranges_match_direct_calls(nb, ragged, monkeypatch):
         assert (d.n_pairs, d.n_entries) == got[k][2:]
 
 
+def test_stream_error_leaves_the_voxelizer_usable():
+    """An invalid primitive in the middle of a stream raises the package's
+    ValueError (after every stream of the call is drained), and the same
+    Voxelizer streams correctly afterwards."""
+    import torch
+    P = _pkg()
+    spec = P.VoxelGridSpec((-8.0, -8.0, -2.0), (40, 40, 16), 0.4)
+    vox = P.Voxelizer(spec, P.VoxelizeConfig(), 6)
+    batches = [_scene(120 + k, 150, C=6, frames=16, origin=spec.origin, dims=spec.dims, smax=2.0)
+               for k in range(4)]
+    bad_scale = np.array(batches[2].scale, copy=True)
+    bad_scale[13, 7, 1] = -1.0
+    bad = P.PrimitiveBatch(batches[2].mu, bad_scale, batches[2].rot, batches[2].opacity,
+                           batches[2].eps, batches[2].logits)
+    pin = lambda b: P.PrimitiveBatch(**{f: torch.from_numpy(np.asarray(getattr(b, f)))
+                                         .pin_memory() for f in P.PrimitiveBatch.FIELDS})
+    # a middle batch (one call) and the last one (run as frame ranges): the
+    # frame index is the batch's either way
+    with pytest.raises(ValueError, match="frame 13 primitive 7"):
+        vox.stream([pin(b) for b in batches[:2]] + [pin(bad), pin(batches[3])])
+    with pytest.raises(ValueError, match="frame 13 primitive 7"):
+        vox.stream([pin(b) for b in batches[:2]] + [pin(bad)])
+    labels = vox.stream([pin(b) for b in batches])
+    for b, lab in zip(batches, labels):
+        assert torch.equal(vox(b).labels.cpu(), lab)
+
+
 def test_truncation_report_soundness():
     """cmd_voxelize --oracle: omitted mass is non-negative,
     every label flip lost mass, and the omitted mass stays under the summed
