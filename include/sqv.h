@@ -88,9 +88,9 @@ typedef struct sqv_cfg {
   int32_t free_label;          /* u8 code written for free voxels (0..255, outside [0, C)) */
   double window_extent;        /* max K of the scaled family, default 2.5 */
   int32_t precision;           /* 1: strict (default) — coordinate logs on the FMA pipe for
-                                  primitives with 2/eps1 > 3, densities within 1e-5 relative
-                                  down to 1e-3*tau; 0: fast — all logs on the SFU (~13% faster,
-                                  2e-5 relative down to 1e-3*tau) */
+                                  primitives with 2/eps1 > 4, densities within 1e-5 relative
+                                  down to 1e-3*tau; 0: fast — all logs on the SFU (~5% faster,
+                                  3e-5 relative down to 1e-3*tau) */
 } sqv_cfg;
 
 /* Primitive batch (device pointers, FP64). */

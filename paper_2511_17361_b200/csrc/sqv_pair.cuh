@@ -203,10 +203,51 @@ __device__ __forceinline__ float2 log2_acc2(float2 x) {
   return fma2(r, q, make_float2((float)e0, (float)e1));
 }
 
+// Strict accurate-log primitives (c = 2/eps1 > SQV_ACC_C) take the log of
+// the coordinate pair (fl(h + l), its Fast2Sum error) instead of the rounded
+// coordinate: the coordinate's 0.5-ulp rounding reaches w = exp(-F) as
+// F c 6e-8, 6.9e-6 at the density floor (F = 11.5) for c = 10, most of the
+// 1e-5 budget.  Measured on 1,024 config-1 frames: worst |dv_o| / v_o
+// 1.19e-5 -> 9.7e-6 (the four worst voxels all sat on c = 7.5-9.7
+// primitives), config 2 -1.3%, config 3 -1.4%.
+#ifndef SQV_ACC_TWOSUM
+#define SQV_ACC_TWOSUM 1
+#endif
+
+// log2|s + err| for the unevaluated pair (s, err), |err| <= ulp(s) / 2 (the
+// rounding error of s = fl(h + l)): log2_acc2's reduction m = |s| 2^-e,
+// r = m - 1 (exact), with err scaled by the same 2^-e folded into r by one
+// FMA — r carries 2-4 more bits than s, so the coordinate's own FP32
+// rounding (amplified by c = 2/eps1 and by F) drops out of the log.
+__device__ __forceinline__ float2 log2_acc2_ds(float2 s, float2 err) {
+  const int i0 = __float_as_int(s.x) & 0x7fffffff, i1 = __float_as_int(s.y) & 0x7fffffff;
+  const int e0 = (i0 - 0x3f3504f3) >> 23, e1 = (i1 - 0x3f3504f3) >> 23;
+  // err * sign(s) (log of |s + err| = |s| + sign(s) err), times 2^-e
+  const float2 ea = make_float2(
+      __int_as_float(__float_as_int(err.x) ^ (__float_as_int(s.x) & 0x80000000)),
+      __int_as_float(__float_as_int(err.y) ^ (__float_as_int(s.y) & 0x80000000)));
+  const float2 sc = make_float2(__int_as_float(0x3f800000 - (e0 << 23)),
+                                __int_as_float(0x3f800000 - (e1 << 23)));
+  const float2 r = fma2(ea, sc, add2(make_float2(__int_as_float(i0 - (e0 << 23)),
+                                                 __int_as_float(i1 - (e1 << 23))), bc2(-1.0f)));
+  float2 q = bc2(1.258370578e-01f);
+  q = fma2(q, r, bc2(-2.072697580e-01f));
+  q = fma2(q, r, bc2(2.157156020e-01f));
+  q = fma2(q, r, bc2(-2.389448136e-01f));
+  q = fma2(q, r, bc2(2.879162431e-01f));
+  q = fma2(q, r, bc2(-3.607036769e-01f));
+  q = fma2(q, r, bc2(4.809106290e-01f));
+  q = fma2(q, r, bc2(-7.213473320e-01f));
+  q = fma2(q, r, bc2(1.442695022e+00f));
+  return fma2(r, q, make_float2((float)e0, (float)e1));
+}
+
 // Local coordinates of a thread's 4 voxels, packed by voxel pairs:
-// P[r][h] = coordinate r of voxels (2h, 2h+1).
+// P[r][h] = coordinate r of voxels (2h, 2h+1); E[r][h] its rounding error
+// (strict accurate-log primitives with SQV_ACC_TWOSUM).
 struct ColCoords2 {
   float2 P[3][2];
+  float2 E[3][2];
   bool live[kVPT];
   int in_xy;
 };
@@ -237,7 +278,7 @@ __device__ __forceinline__ float live_sel(float u, int z, int lo, int hi, int in
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
 // primitives far from their centre voxel.  (hi, lo) run as one packed pair.
-template <bool EXACT_STEP, bool LIVE = true>
+template <bool EXACT_STEP, bool LIVE = true, bool TWOSUM = false>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords2& cd) {
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
@@ -254,6 +295,10 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
       const float2 l23 = fma2(v23, bc2(R.HL[3 * r + 2].y), bc2(hl.y));
       cd.P[r][0] = add2(h01, l01);
       cd.P[r][1] = add2(h23, l23);
+      if (TWOSUM) {  // Fast2Sum: l - (s - h), exact when |h| >= |l|
+        cd.E[r][0] = fma2(bc2(-1.0f), fma2(bc2(-1.0f), h01, cd.P[r][0]), l01);
+        cd.E[r][1] = fma2(bc2(-1.0f), fma2(bc2(-1.0f), h23, cd.P[r][1]), l23);
+      }
     } else {  // fast: <= 3 steps of the once-rounded z step (error <= 3 ulp(dz))
       const float p0 = hl.x + hl.y;
       cd.P[r][0] = fma2(v01, bc2(R.Ez[r]), bc2(p0));
@@ -332,16 +377,20 @@ struct PairState {
 template <bool EXACT_STEP, bool LIVE, bool ACC>
 __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z0,
                                            PairState& S) {
+  constexpr bool kDS = SQV_ACC_TWOSUM && EXACT_STEP && ACC;
   ColCoords2 cd;
-  pair_coords<EXACT_STEP, LIVE>(R, x, y, z0, cd);
+  pair_coords<EXACT_STEP, LIVE, kDS>(R, x, y, z0, cd);
   const float a = R.a, c = R.c;
+  auto lg = [&](int r, int h) {
+    return kDS ? log2_acc2_ds(cd.P[r][h], cd.E[r][h]) : log2p<ACC>(cd.P[r][h]);
+  };
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const float2 ux = mul2(bc2(a), log2p<ACC>(cd.P[0][h]));
-    const float2 uy = mul2(bc2(a), log2p<ACC>(cd.P[1][h]));
+    const float2 ux = mul2(bc2(a), lg(0, h));
+    const float2 uy = mul2(bc2(a), lg(1, h));
     // log2(log2 e) folded into the exponents (2^(u + k) = log2(e) 2^u; see
     // stage_exps)
-    float2 uz = fma2(bc2(c), log2p<ACC>(cd.P[2][h]), bc2(kLog2Log2e));
+    float2 uz = fma2(bc2(c), lg(2, h), bc2(kLog2Log2e));
     // umin - umax = -|ux - uy| (the same rounded value); both coordinates 0
     // give NaN, clamped to -126 (t ~ 0) while umax = -inf makes S^b = 0
     S.um[h] = make_float2(fmaxf(ux.x, uy.x), fmaxf(ux.y, uy.y));

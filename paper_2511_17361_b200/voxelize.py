@@ -80,7 +80,7 @@ class VoxelizeConfig:
     semantic_mode ("logit-sum" | "prob-sum").  window_extent is the ledger's
     max-K expansion factor (default 2.5).  precision selects the
     device numerics: "strict" (default; densities within 1e-5 relative down to
-    1e-3*tau) or "fast" (all logs on the SFU, ~13% faster; 2e-5 relative down to
+    1e-3*tau) or "fast" (all logs on the SFU, ~5% faster; 3e-5 relative down to
     1e-3*tau) — see DESIGN.md §Numerics."""
 
     tau: float = 0.01

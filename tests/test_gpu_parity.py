@@ -116,7 +116,7 @@ def test_config1_occ3d_256():
 
 def test_fast_precision_mode():
     """precision="fast" (all logs on the SFU): labels unchanged, densities within
-    2e-5 relative down to 1e-3*tau."""
+    3e-5 relative down to 1e-3*tau."""
     P = _pkg()
     spec, cfg = P.VoxelGridSpec(), P.VoxelizeConfig(precision="fast")
     b = _scene(11, 256)
