@@ -204,32 +204,29 @@ __device__ __forceinline__ float2 log2_acc2(float2 x) {
 }
 
 // Strict accurate-log primitives (c = 2/eps1 > SQV_ACC_C) take the log of
-// the coordinate pair (fl(h + l), its Fast2Sum error) instead of the rounded
-// coordinate: the coordinate's 0.5-ulp rounding reaches w = exp(-F) as
-// F c 6e-8, 6.9e-6 at the density floor (F = 11.5) for c = 10, most of the
-// 1e-5 budget.  Measured on 1,024 config-1 frames: worst |dv_o| / v_o
-// 1.19e-5 -> 9.7e-6 (the four worst voxels all sat on c = 7.5-9.7
-// primitives), config 2 -1.3%, config 3 -1.4%.
+// the coordinate's parts (log2_acc2_hl) instead of the rounded coordinate:
+// the coordinate's 0.5-ulp rounding reaches w = exp(-F) as F c 6e-8, 6.9e-6
+// at the density floor (F = 11.5) for c = 10, most of the 1e-5 budget.
+// Measured on 1,024 config-1 frames: worst |dv_o| / v_o 1.19e-5 -> 9.7e-6
+// (the four worst voxels all sat on c = 7.5-9.7 primitives); config 2
+// -1.15%, config 3 -0.85% (a Fast2Sum form of the same fold: -1.3%/-1.4%).
 #ifndef SQV_ACC_TWOSUM
 #define SQV_ACC_TWOSUM 1
 #endif
 
-// log2|s + err| for the unevaluated pair (s, err), |err| <= ulp(s) / 2 (the
-// rounding error of s = fl(h + l)): log2_acc2's reduction m = |s| 2^-e,
-// r = m - 1 (exact), with err scaled by the same 2^-e folded into r by one
-// FMA — r carries 2-4 more bits than s, so the coordinate's own FP32
-// rounding (amplified by c = 2/eps1 and by F) drops out of the log.
-__device__ __forceinline__ float2 log2_acc2_ds(float2 s, float2 err) {
+// log2|h + l| of the coordinate's exact parts (h the lattice-exact hi sum,
+// l the lo sum) rather than of its rounding s = fl(h + l): log2_acc2's
+// reduction takes e from s, then r = sign(s) 2^-e h - 1 (exact, Sterbenz)
+// + sign(s) 2^-e l, rounded once, so r carries the coordinate to a fraction
+// of s's ulp.  s = 0 (h = -l, both small) gives r = 0 and the log's floor
+// -127 like log2_acc2.
+__device__ __forceinline__ float2 log2_acc2_hl(float2 s, float2 h, float2 l) {
   const int i0 = __float_as_int(s.x) & 0x7fffffff, i1 = __float_as_int(s.y) & 0x7fffffff;
   const int e0 = (i0 - 0x3f3504f3) >> 23, e1 = (i1 - 0x3f3504f3) >> 23;
-  // err * sign(s) (log of |s + err| = |s| + sign(s) err), times 2^-e
-  const float2 ea = make_float2(
-      __int_as_float(__float_as_int(err.x) ^ (__float_as_int(s.x) & 0x80000000)),
-      __int_as_float(__float_as_int(err.y) ^ (__float_as_int(s.y) & 0x80000000)));
-  const float2 sc = make_float2(__int_as_float(0x3f800000 - (e0 << 23)),
-                                __int_as_float(0x3f800000 - (e1 << 23)));
-  const float2 r = fma2(ea, sc, add2(make_float2(__int_as_float(i0 - (e0 << 23)),
-                                                 __int_as_float(i1 - (e1 << 23))), bc2(-1.0f)));
+  const float2 sc = make_float2(
+      __int_as_float((0x3f800000 - (e0 << 23)) | (__float_as_int(s.x) & 0x80000000)),
+      __int_as_float((0x3f800000 - (e1 << 23)) | (__float_as_int(s.y) & 0x80000000)));
+  const float2 r = fma2(l, sc, fma2(h, sc, bc2(-1.0f)));
   float2 q = bc2(1.258370578e-01f);
   q = fma2(q, r, bc2(-2.072697580e-01f));
   q = fma2(q, r, bc2(2.157156020e-01f));
@@ -243,11 +240,11 @@ __device__ __forceinline__ float2 log2_acc2_ds(float2 s, float2 err) {
 }
 
 // Local coordinates of a thread's 4 voxels, packed by voxel pairs:
-// P[r][h] = coordinate r of voxels (2h, 2h+1); E[r][h] its rounding error
-// (strict accurate-log primitives with SQV_ACC_TWOSUM).
+// P[r][h] = coordinate r of voxels (2h, 2h+1); H, L its hi and lo parts
+// (strict accurate-log primitives, SQV_ACC_TWOSUM).
 struct ColCoords2 {
   float2 P[3][2];
-  float2 E[3][2];
+  float2 H[3][2], L[3][2];
   bool live[kVPT];
   int in_xy;
 };
@@ -295,9 +292,11 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
       const float2 l23 = fma2(v23, bc2(R.HL[3 * r + 2].y), bc2(hl.y));
       cd.P[r][0] = add2(h01, l01);
       cd.P[r][1] = add2(h23, l23);
-      if (TWOSUM) {  // Fast2Sum: l - (s - h), exact when |h| >= |l|
-        cd.E[r][0] = fma2(bc2(-1.0f), fma2(bc2(-1.0f), h01, cd.P[r][0]), l01);
-        cd.E[r][1] = fma2(bc2(-1.0f), fma2(bc2(-1.0f), h23, cd.P[r][1]), l23);
+      if (TWOSUM) {  // the exact parts, for log2_acc2_hl
+        cd.H[r][0] = h01;
+        cd.H[r][1] = h23;
+        cd.L[r][0] = l01;
+        cd.L[r][1] = l23;
       }
     } else {  // fast: <= 3 steps of the once-rounded z step (error <= 3 ulp(dz))
       const float p0 = hl.x + hl.y;
@@ -382,7 +381,7 @@ __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z
   pair_coords<EXACT_STEP, LIVE, kDS>(R, x, y, z0, cd);
   const float a = R.a, c = R.c;
   auto lg = [&](int r, int h) {
-    return kDS ? log2_acc2_ds(cd.P[r][h], cd.E[r][h]) : log2p<ACC>(cd.P[r][h]);
+    return kDS ? log2_acc2_hl(cd.P[r][h], cd.H[r][h], cd.L[r][h]) : log2p<ACC>(cd.P[r][h]);
   };
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
