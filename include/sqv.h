@@ -25,8 +25,9 @@
  *   - Return value: SQV_OK (0) or a negative SQV_ERR_* code; a message is
  *     available from sqv_last_error() (thread-local).
  *   - The library never allocates device memory and keeps no global mutable
- *     state besides the thread-local error string, a launch counter and the
- *     opt-in stage profiler (sqv_profile_*).
+ *     state besides the thread-local error string, a launch counter, the
+ *     opt-in stage profiler (sqv_profile_*) and the optional work-counter
+ *     pointer (sqv_stats_attach) — instrumentation, process-wide.
  *     Scratch comes from the caller's workspace pointer.
  *   - Results are deterministic: identical inputs give bit-identical outputs
  *      regardless of batch composition or GPU count.
