@@ -1,7 +1,7 @@
 """End-to-end fixed cost of Voxelizer.stream (GPU box): t(K) for K pinned
 100-frame config-2 batches, labels back to the host, with and without the
 edge ranges (first/last batch split in frame ranges).  Best of 3 per point,
-the two settings interleaved.  usage: python scripts/e2e_fixed_cost.py"""
+the two settings interleaved.  usage: python scripts/e2e_fixed_cost.py [edge piece counts, default 1,4]"""
 import os
 import sys
 
@@ -20,7 +20,8 @@ pinned = [P.PrimitiveBatch(**{k: torch.from_numpy(np.ascontiguousarray(getattr(b
 labels = [torch.empty((100, 16, 200, 200), dtype=torch.uint8).pin_memory() for _ in range(20)]
 dev = [vox.to_device(b) for b in pinned]
 outs = [vox.alloc(100), vox.alloc(100)]
-for e in (1, 4):
+EDGES = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 4]
+for e in EDGES:
     vox.stream(pinned[:2], labels_out=labels[:2], edge_pieces=e)
 vox.run_many(dev[:2], outs)
 torch.cuda.synchronize()
@@ -43,8 +44,7 @@ for K in (1, 2, 4, 10, 20):
     seq = [pinned[k % 4] for k in range(K)]
     d = timed(lambda: vox.run_many([dev[k % 4] for k in range(K)], outs))
     row = {"K": K, "device_resident_ms": round(d, 3)}
-    for e in (1, 4):
+    for e in EDGES:
         row[f"edge{e}_ms"] = round(timed(lambda: vox.stream(seq, labels_out=labels[:K],
                                                              edge_pieces=e)), 3)
-    row["edge4_gain"] = round(row["edge1_ms"] / row["edge4_ms"] - 1, 4)
     print(row, flush=True)
