@@ -3,7 +3,8 @@ configs' own generator (scenegen.gen_frames, the bench seed and grids)
 voxelized by the product path in both precisions, every frame checked in
 full against the FP64 oracle (oracle/, the checker): bins and pair counts
 exact, the worst |dv_o| / max(v_o, floor), the worst v_c error against the
-voxel's weight scale, label agreement and unexplained mismatches
+voxel's weight scale (with the term magnitudes sum_i w_i |c_ik| from an
+oracle run on |logits|), label agreement and unexplained mismatches
 (tests/parity.py rules).  Frames run in chunks (the oracle's FP64 v_c of a
 config-4 frame is 0.7 GB).  Writes gpurun_out/parity_sweep.json.
 
@@ -23,8 +24,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_2511_17361_b200 as P  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2511_17361_b200.scenegen import gen_frames  # noqa: E402
-from parity import (VO_MIN_FLOOR, VO_REL, VO_REL_TAIL, VO_TAIL_FLOOR_FRAC_TAU,  # noqa: E402
-                    label_check, vo_check)
+from parity import VO_REL, VO_REL_TAIL, label_check, vo_check, weight_scale  # noqa: E402
 
 SEED = 20251117  # bench.py default
 OCC = dict(origin=(-40.0, -40.0, -1.0), dims=(200, 200, 16), resolution=0.4)
@@ -38,9 +38,8 @@ CONFIGS = {  # name: (frames, chunk, n_prims, grid, gen kwargs) — bench.py WOR
 }
 
 
-def vc_worst(vc_g, vc_r, vo_r, tau):
-    floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
-    scale = np.maximum(np.maximum(np.abs(vc_r).max(axis=-1), vo_r), floor)
+def vc_worst(vc_g, vc_r, vo_r, tau, vc_abs):
+    scale = weight_scale(vo_r, vc_r, tau, vc_abs).reshape(vc_r.shape[:-1])
     return float((np.abs(vc_g.astype(np.float64) - vc_r).max(axis=-1) / scale).max(initial=0.0))
 
 
@@ -63,8 +62,12 @@ def main():
             b = gen_frames(SEED, nf, N, 18, first_frame=f0, origin=spec.origin, dims=spec.dims,
                            resolution=spec.resolution, **kw)
             t0 = time.perf_counter()
-            ref = O.voxelize(O.Prims.of(b), grid, O.Cfg(free_label=255))
+            p = O.Prims.of(b)
+            ref = O.voxelize(p, grid, O.Cfg(free_label=255))
             t_ref = time.perf_counter() - t0
+            # the class sums' term magnitudes sum_i w_i |c_ik| (tests/parity.py)
+            vc_abs = O.voxelize(O.Prims(p.mu, p.scale, p.rot, p.opacity, p.eps, np.abs(p.logits),
+                                        p.n_valid), grid, O.Cfg(free_label=255))["v_c"]
             win = O.prep(O.Prims.of(b), grid, O.Cfg(free_label=255))
             off, ids = O.bins(win, grid.dims)
             C = ref["v_c"].shape[-1]
@@ -85,8 +88,9 @@ def main():
                 a["worst_vo_rel"] = max(a["worst_vo_rel"], v["worst_rel"])
                 a["n_vo_out_of_bound"] += v["n_bad"]
                 a["worst_vc_rel"] = max(a["worst_vc_rel"], vc_worst(vc, ref["v_c"], ref["v_o"],
-                                                                    cfg.tau))
-                lc = label_check(lab, ref["labels"], ref["v_o"], ref["v_c"], cfg.tau, r.free_code)
+                                                                    cfg.tau, vc_abs))
+                lc = label_check(lab, ref["labels"], ref["v_o"], ref["v_c"], cfg.tau, r.free_code,
+                                 vc_abs)
                 a["n_label_mismatch"] += lc["n_mismatch"]
                 a["n_unexplained"] += lc["n_unexplained"]
                 a["n_resolvable"] += lc["n_resolvable"]
@@ -94,7 +98,7 @@ def main():
                 a["voxels"] += int(lab.size)
                 a["frames"] += nf
                 a["oracle_s"] += t_ref
-            del ref
+            del ref, vc_abs
         for prec, a in acc.items():
             a["label_agreement"] = 1.0 - a["n_resolvable_mismatch"] / max(a["n_resolvable"], 1)
             a["vc_limit"] = 2 * (VO_REL if prec == "strict" else VO_REL_TAIL)

@@ -18,13 +18,16 @@
                                                4,096 config-1 frames measured
                                                2.2e-5);
 * class sums v_c: twice the v_o bound per mode, against the voxel's weight
-  scale max(max_k |v_c,k|, v_o, floor) — with mixed-sign logits cancelling
-  inside v_c and sigma < 1 that scale is only a lower bound of the term
-  magnitude sum_i w_i |c_i|;
+  scale max(max_k T_k, max_k |v_c,k|, v_o, floor), T_k = sum_i w_i |c_ik|
+  the term magnitude of class k (the oracle run with |logits|, ref["v_c_abs"],
+  when the caller has it): every term w_i c_ik carries the relative error of
+  w_i, so |dv_c,k| scales with T_k, and with mixed-sign logits cancelling
+  inside v_c (and sigma < 1 under v_o) max(|v_c|, v_o) alone can be far
+  below it;
 * labels: a voxel may disagree only where the oracle's top-2 class scores
   differ by < LABEL_GAP * scale + 2 * CULL_DROP, scale being the voxel's
-  weight scale of the v_c check (max(max_k |v_c,k|, v_o, floor): relative to
-  the voxel's own term magnitude, no absolute floor of 1), or where the
+  weight scale of the v_c check (relative to the voxel's own term
+  magnitude, no absolute floor of 1), or where the
   oracle's v_o lies within VO_REL of tau (a tau flip).  CULL_DROP is the
   block cull's per-voxel bound on the dropped mass: every
   class sum moves by < 2e-12, so a top-2 gap below twice that can flip.
@@ -65,13 +68,25 @@ def vo_check(gpu, ref, tau, mode="strict"):
     return out
 
 
-def label_check(gpu_lab, ref_lab, ref_vo, ref_vc, tau, free_code):
+def weight_scale(ref_vo, ref_vc, tau, ref_vc_abs=None):
+    """Per voxel: max(max_k T_k, max_k |v_c,k|, v_o, floor) (see above)."""
+    C = ref_vc.shape[-1]
+    vc = np.abs(np.asarray(ref_vc, np.float64)).reshape(-1, C).max(axis=-1)
+    vo = np.asarray(ref_vo, np.float64).ravel()
+    floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
+    s = np.maximum(np.maximum(vc, vo), floor)
+    if ref_vc_abs is not None:
+        s = np.maximum(s, np.asarray(ref_vc_abs, np.float64).reshape(-1, C).max(axis=-1))
+    return s
+
+
+def label_check(gpu_lab, ref_lab, ref_vo, ref_vc, tau, free_code, ref_vc_abs=None):
     g = np.asarray(gpu_lab).ravel()
     r = np.asarray(ref_lab).ravel()
     vo = np.asarray(ref_vo, np.float64).ravel()
     C = ref_vc.shape[-1]
     vc = np.asarray(ref_vc, np.float64).reshape(-1, C)
-    floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
+    wscale = weight_scale(ref_vo, ref_vc, tau, ref_vc_abs)
     mism = np.flatnonzero(g != r)
     unexplained = []
     for v in mism:
@@ -79,8 +94,7 @@ def label_check(gpu_lab, ref_lab, ref_vo, ref_vc, tau, free_code):
             continue  # tau flip
         if g[v] != free_code and r[v] != free_code:
             top = vc[v, r[v]]
-            scale = max(np.abs(vc[v]).max(), vo[v], floor)
-            if top - vc[v, g[v]] <= LABEL_GAP * scale + 2 * CULL_DROP:
+            if top - vc[v, g[v]] <= LABEL_GAP * wscale[v] + 2 * CULL_DROP:
                 continue  # near-tie in the oracle's scores
         unexplained.append(int(v))
     resolvable = vo > CULL_DROP
@@ -96,21 +110,19 @@ def assert_parity(gpu, ref, tau, free_code, check_vc=True, mode="strict",
     """gpu/ref: dicts with v_o [F,V], v_c [F,V,C] (ref FP64), labels [F,V]."""
     vo = vo_check(gpu["v_o"], ref["v_o"], tau, mode)
     assert vo["n_bad"] == 0, f"v_o out of tolerance: {vo}"
-    lab = label_check(gpu["labels"], ref["labels"], ref["v_o"], ref["v_c"], tau, free_code)
+    vc_abs = ref.get("v_c_abs")
+    lab = label_check(gpu["labels"], ref["labels"], ref["v_o"], ref["v_c"], tau, free_code,
+                      vc_abs)
     assert lab["n_unexplained"] == 0, f"unexplained label mismatches: {lab}"
     assert lab["agreement"] >= min_agreement, lab
     if check_vc:
-        # class weights: absolute error relative to the voxel's weight scale,
-        # max(|v_c|, v_o) — v_o = sum(sigma w) bounds sum(w) from below, so it
-        # stands for the term magnitude when mixed-sign logits cancel in v_c
+        # class sums against the voxel's weight scale (the term magnitude
+        # when ref carries v_c_abs); twice the v_o bound: the B operand's
+        # 3xTF32 split and the class weights' own rounding add to w's error
         vc_g = np.asarray(gpu["v_c"], np.float64)
         vc_r = np.asarray(ref["v_c"], np.float64)
-        vo_r = np.asarray(ref["v_o"], np.float64).reshape(vc_r.shape[:-1] + (1,))
-        floor = max(VO_TAIL_FLOOR_FRAC_TAU * tau, VO_MIN_FLOOR)
-        scale = np.maximum(np.maximum(np.abs(vc_r).max(axis=-1, keepdims=True), vo_r), floor)
+        scale = weight_scale(ref["v_o"], vc_r, tau, vc_abs).reshape(vc_r.shape[:-1] + (1,))
         rel = np.abs(vc_g - vc_r) / scale
-        # twice the v_o bound: max(|v_c|, v_o) only bounds the term magnitude
-        # sum(w |c|) from below when mixed-sign logits cancel (and sigma < 1)
         lim = 2 * (VO_REL if mode == "strict" else VO_REL_TAIL)
         assert float(rel.max(initial=0.0)) <= lim, f"v_c worst {float(rel.max())}"
     return vo, lab

@@ -51,6 +51,10 @@ def _oracle(batch, spec, cfg, free_code, truncate=True):
               free_code, cfg.window_extent)
     r = O.voxelize(p, grid, c)
     r["windows"] = O.prep(p, grid, c)
+    if cfg.semantic_mode == "logit-sum":
+        # the class sums' term magnitudes sum_i w_i |c_ik| (parity.weight_scale)
+        pa = O.Prims(p.mu, p.scale, p.rot, p.opacity, p.eps, np.abs(p.logits), p.n_valid)
+        r["v_c_abs"] = O.voxelize(pa, grid, c)["v_c"]
     return r, grid
 
 
