@@ -210,8 +210,8 @@ __device__ __forceinline__ float2 log2_acc2(float2 x) {
 // Measured on 1,024 config-1 frames: worst |dv_o| / v_o 1.19e-5 -> 9.7e-6
 // (the four worst voxels all sat on c = 7.5-9.7 primitives); config 2
 // -1.15%, config 3 -0.85% (a Fast2Sum form of the same fold: -1.3%/-1.4%).
-#ifndef SQV_ACC_TWOSUM
-#define SQV_ACC_TWOSUM 1
+#ifndef SQV_ACC_PARTS
+#define SQV_ACC_PARTS 1
 #endif
 
 // log2|h + l| of the coordinate's exact parts (h the lattice-exact hi sum,
@@ -241,7 +241,7 @@ __device__ __forceinline__ float2 log2_acc2_hl(float2 s, float2 h, float2 l) {
 
 // Local coordinates of a thread's 4 voxels, packed by voxel pairs:
 // P[r][h] = coordinate r of voxels (2h, 2h+1); H, L its hi and lo parts
-// (strict accurate-log primitives, SQV_ACC_TWOSUM).
+// (strict accurate-log primitives, SQV_ACC_PARTS).
 struct ColCoords2 {
   float2 P[3][2];
   float2 H[3][2], L[3][2];
@@ -275,7 +275,7 @@ __device__ __forceinline__ float live_sel(float u, int z, int lo, int hi, int in
 // quantum) times small integer offsets sum exactly in FP32, the lo parts are
 // small, so x' carries no cancellation error even for thin, rotated
 // primitives far from their centre voxel.  (hi, lo) run as one packed pair.
-template <bool EXACT_STEP, bool LIVE = true, bool TWOSUM = false>
+template <bool EXACT_STEP, bool LIVE = true, bool PARTS = false>
 __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int z0,
                                             ColCoords2& cd) {
   const float fx = (float)x - R.cx, fy = (float)y - R.cy, fz = (float)z0 - R.cz;
@@ -292,7 +292,7 @@ __device__ __forceinline__ void pair_coords(const PrimRec& R, int x, int y, int 
       const float2 l23 = fma2(v23, bc2(R.HL[3 * r + 2].y), bc2(hl.y));
       cd.P[r][0] = add2(h01, l01);
       cd.P[r][1] = add2(h23, l23);
-      if (TWOSUM) {  // the exact parts, for log2_acc2_hl
+      if (PARTS) {  // the exact parts, for log2_acc2_hl
         cd.H[r][0] = h01;
         cd.H[r][1] = h23;
         cd.L[r][0] = l01;
@@ -376,12 +376,12 @@ struct PairState {
 template <bool EXACT_STEP, bool LIVE, bool ACC>
 __device__ __forceinline__ void stage_logs(const PrimRec& R, int x, int y, int z0,
                                            PairState& S) {
-  constexpr bool kDS = SQV_ACC_TWOSUM && EXACT_STEP && ACC;
+  constexpr bool kParts = SQV_ACC_PARTS && EXACT_STEP && ACC;
   ColCoords2 cd;
-  pair_coords<EXACT_STEP, LIVE, kDS>(R, x, y, z0, cd);
+  pair_coords<EXACT_STEP, LIVE, kParts>(R, x, y, z0, cd);
   const float a = R.a, c = R.c;
   auto lg = [&](int r, int h) {
-    return kDS ? log2_acc2_hl(cd.P[r][h], cd.H[r][h], cd.L[r][h]) : log2p<ACC>(cd.P[r][h]);
+    return kParts ? log2_acc2_hl(cd.P[r][h], cd.H[r][h], cd.L[r][h]) : log2p<ACC>(cd.P[r][h]);
   };
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
