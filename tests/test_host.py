@@ -208,3 +208,41 @@ def test_torch_ops_registered_with_fake_shapes():
     with pytest.raises(RuntimeError):
         torch.ops.sqocc.voxelize(z(F, N, 3), z(F, N, 3), z(F, N, 4), z(F, N), z(F, N, 2),
                                  z(F, N, C), [-40.0, -40.0, -1.0], [200, 200, 16], 0.4)
+
+
+def test_parity_rules_scale_with_the_term_magnitude():
+    """tests/parity.py: the v_c check and the near-tie rule scale with the
+    class term magnitude sum_i w_i |c_ik| when the oracle supplies it, so a
+    class sum that cancels (v_c ~ 0 from large opposite terms) is judged
+    against its terms, not against itself."""
+    import parity as PR
+    tau = 0.01
+    ref_vo = np.array([[6.9e-5, 0.5]])
+    ref_vc = np.array([[[-1.65e-5], [0.3]]])          # voxel 0 cancels: |v_c| << terms
+    vc_abs = np.array([[[4.0e-4], [0.3]]])           # sum_i w_i |c_i|
+    s0 = PR.weight_scale(ref_vo, ref_vc, tau)
+    s1 = PR.weight_scale(ref_vo, ref_vc, tau, vc_abs)
+    np.testing.assert_allclose(s0, [6.9e-5, 0.5])
+    np.testing.assert_allclose(s1, [4.0e-4, 0.5])
+    # an error of 1.6e-9 on the cancelling sum: 2.3e-5 of the lower bound
+    # (fails 2e-5), 4e-6 of the term magnitude (passes)
+    gpu = {"v_o": ref_vo.astype(np.float32), "v_c": ref_vc + np.array([[[1.6e-9], [0.0]]]),
+           "labels": np.array([[0, 0]], np.uint8)}
+    ref = {"v_o": ref_vo, "v_c": ref_vc, "labels": np.array([[0, 0]], np.uint8)}
+    with pytest.raises(AssertionError, match="v_c worst"):
+        PR.assert_parity(gpu, ref, tau, free_code=1, min_agreement=0.0)
+    PR.assert_parity(gpu, dict(ref, v_c_abs=vc_abs), tau, free_code=1, min_agreement=0.0)
+    # near-tie rule: a 2-class voxel may flip only when its top-2 gap is
+    # below 1e-5 of its scale (3e-5 here, 2e-3 with the term magnitude)
+    vc2 = np.array([[[2.0e-5, 2.0e-5 - 1e-10]]])
+    lab = PR.label_check(np.array([[1]], np.uint8), np.array([[0]], np.uint8),
+                         np.array([[3e-5]]), vc2, tau, free_code=2)
+    assert lab["n_unexplained"] == 0
+    vc3 = np.array([[[2.0e-5, 2.0e-5 - 1e-8]]])
+    lab = PR.label_check(np.array([[1]], np.uint8), np.array([[0]], np.uint8),
+                         np.array([[3e-5]]), vc3, tau, free_code=2)
+    assert lab["n_unexplained"] == 1
+    lab = PR.label_check(np.array([[1]], np.uint8), np.array([[0]], np.uint8),
+                         np.array([[3e-5]]), vc3, tau, free_code=2,
+                         ref_vc_abs=np.array([[[2e-3, 2e-3]]]))
+    assert lab["n_unexplained"] == 0
