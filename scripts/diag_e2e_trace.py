@@ -1,5 +1,14 @@
-import os, sys, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+"""Stage timelines (SQV_PROF_TRACE=1) of run_many on device batches and of
+Voxelizer.stream on pinned host batches (GPU box, diagnostics): per call,
+the prep, scan, readback, masks and evaluator events on one clock (stderr).
+usage: SQV_PROF_TRACE=1 python scripts/diag_e2e_trace.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_17361_b200 as P
 from paper_2511_17361_b200 import _lib
 from paper_2511_17361_b200.scenegen import gen_frames
@@ -9,7 +18,9 @@ pinned = [P.PrimitiveBatch(**{k: torch.from_numpy(np.ascontiguousarray(getattr(b
 labels = [torch.empty((100, 16, 200, 200), dtype=torch.uint8).pin_memory() for _ in range(8)]
 dev = [vox.to_device(b) for b in pinned]
 outs = [vox.alloc(100), vox.alloc(100)]
-vox.stream(pinned[:2], labels_out=labels[:2], edge_pieces=1); vox.run_many(dev[:2], outs); torch.cuda.synchronize()
+vox.stream(pinned[:2], labels_out=labels[:2], edge_pieces=1)
+vox.run_many(dev[:2], outs)
+torch.cuda.synchronize()
 K = 6
 for name, fn in (("run_many", lambda: vox.run_many([dev[k % 4] for k in range(K)], outs)),
                  ("stream", lambda: vox.stream([pinned[k % 4] for k in range(K)], labels_out=labels[:K], edge_pieces=1)),
